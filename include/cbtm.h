@@ -1,0 +1,216 @@
+/*
+ * cbtm.h -- C ABI of libcbtm.so: the B200 (sm_100a) implementation of the
+ * per-frame bisector update of arXiv 2407.02215.
+ *
+ * The reference (`cbtmesh`, pure Python + numba) has no FFI of its own; the
+ * seam it offers is its Python API.  Each entry point below names the reference
+ * interface it stands in for (paths relative to /root/reference/pkg/src/cbtmesh).
+ * INTEGRATION.md shows the ctypes binding a maintainer would add.
+ *
+ * Conventions
+ *   - extern "C", plain pointers and sizes only.  Unless stated otherwise every
+ *     pointer is a DEVICE pointer owned by the caller; `stream` is a
+ *     cudaStream_t passed as uintptr_t (0 = default stream).
+ *   - Calls are asynchronous on `stream`, never synchronise the host, never
+ *     allocate device memory (scratch is caller-provided, sized by
+ *     cbtm_workspace_bytes) and never throw.
+ *   - Return value: 0 ok; < 0 is -(cudaError_t); > 0 is a CBTM_E_* contract
+ *     violation detected on the host before anything was launched.
+ *   - There is no CPU fallback.  Without a CUDA device every compute entry
+ *     point fails with a negative status.
+ *
+ * CBT storage: a packed bitfield, 1 bit per pool slot (bit s of
+ * the field = slot s; little-endian inside 64-bit words), plus 32-bit counters
+ * for every tree node that spans >= 1024 slots, laid out as a binary heap:
+ * node i of level l (root = level 0) lives at counters[(1 << l) + i].  The
+ * deepest counter level is Lc = max(D - 10, 0); below it a node is a 128-byte
+ * line of the bitfield and is resolved with popcounts.
+ */
+#ifndef CBTM_H_
+#define CBTM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CBTM_ABI_VERSION 1
+#define CBTM_MIN_DEPTH 1
+#define CBTM_MAX_DEPTH 30 /* slot indices are int32; counters are uint32 */
+#define CBTM_LEAF_BLOCK_LOG2 10
+#define CBTM_STATS_WORDS 16
+#define CBTM_PRM_WORDS 23
+
+/* contract violations */
+#define CBTM_E_DEPTH 1     /* depth outside [CBTM_MIN_DEPTH, CBTM_MAX_DEPTH] */
+#define CBTM_E_NULL 2      /* a required pointer is NULL */
+#define CBTM_E_WORKSPACE 3 /* workspace smaller than cbtm_workspace_bytes */
+#define CBTM_E_MODE 4      /* unknown verdict mode / flag */
+#define CBTM_E_RANGE 5     /* count / size argument out of range */
+
+/* command-word bits (state.py:17-25) */
+#define CBTM_CMD_SPLIT_T 1u
+#define CBTM_CMD_SPLIT_N 2u
+#define CBTM_CMD_SPLIT_P 4u
+#define CBTM_CMD_SPLIT_MASK 7u
+#define CBTM_CMD_MERGE 8u
+#define CBTM_CMD_QUAD 16u
+#define CBTM_CMD_OWNER 32u
+
+/* cbtm_pool.flags */
+#define CBTM_POOL_FULL_FREE_CACHE 1u /* materialise cache_free[0, F) every frame
+                                        (whole-array parity with the reference);
+                                        default: only the consumed window
+                                        cache_free[T - A, T) is written */
+
+/* stats layout written by cbtm_update to cbtm_pool.stats (int64) */
+enum {
+    CBTM_STAT_OOM_SPLITS = 0,  /* UpdateStats.splits_rejected_oom */
+    CBTM_STAT_OOM_MERGES = 1,  /* UpdateStats.merges_rejected_oom */
+    CBTM_STAT_SPLIT_FREED = 2, /* UpdateStats.splits_applied      */
+    CBTM_STAT_MERGE_FREED = 3, /* UpdateStats.merges_applied      */
+    CBTM_STAT_SPLIT_ALLOC = 4, /* UpdateStats.split_allocs        */
+    CBTM_STAT_MERGE_ALLOC = 5, /* UpdateStats.merge_allocs        */
+    CBTM_STAT_LIVE_BEFORE = 6,
+    CBTM_STAT_LIVE_AFTER = 7,
+    CBTM_STAT_RESERVED = 8,  /* T: slots reserved by admitted commands   */
+    CBTM_STAT_ALLOCATED = 9, /* A: slots actually allocated              */
+    CBTM_STAT_POISON = 10,   /* fresh pointers resolved to the poison -2 */
+    CBTM_STAT_FRAME = 11     /* frames applied to this pool so far       */
+};
+
+/* One bisector pool == the reference's TriangulationState (state.py:32-55).
+ * Array shapes, N = 2^depth:
+ *   ids u64[N]; nexts/prevs/twins i32[N] (-1 = null); commands u32[N];
+ *   reserved i32[N*4]; cache_live/cache_free i32[N]; counter i64[1];
+ *   bits u64[cbtm_bitfield_words(depth)]; counters u32[cbtm_counter_words(depth)];
+ *   stats i64[CBTM_STATS_WORDS]; dispatch u32[4] = {ceil(n/256), 1, 1, n}
+ *   (indirect-dispatch arguments for the consumer of cache_live; may be NULL). */
+typedef struct cbtm_pool {
+    uint64_t *ids;
+    int32_t *nexts;
+    int32_t *prevs;
+    int32_t *twins;
+    uint32_t *commands;
+    int32_t *reserved;
+    int32_t *cache_live;
+    int32_t *cache_free;
+    int64_t *counter;
+    uint64_t *bits;
+    uint32_t *counters;
+    int64_t *stats;
+    uint32_t *dispatch;
+    void *workspace;
+    size_t workspace_bytes;
+    int32_t depth;     /* D, pool capacity 2^D */
+    int32_t rank;      /* R = max(1, ceil(log2 H)): root ids are 2^R + h */
+    int32_t max_depth; /* split demotion limit (state.max_depth, 63 - R) */
+    uint32_t flags;    /* CBTM_POOL_* */
+} cbtm_pool;
+
+/* Verdict source for stage 4 (pipeline.py:87-119, lod.py:272-312). */
+enum {
+    CBTM_VERDICT_CONST = 0,    /* KeepAll / SplitAll / MergeAll: value = 0/1/2 */
+    CBTM_VERDICT_UNIFORM = 1,  /* UniformSplit: value = target depth           */
+    CBTM_VERDICT_LOD = 2,      /* LodDecide: prm + root_tris                   */
+    CBTM_VERDICT_EXPLICIT = 3  /* int8 verdicts[count] in cache_live order     */
+};
+
+typedef struct cbtm_verdict {
+    int32_t mode;
+    int32_t value;
+    const int8_t *explicit_verdicts; /* device, mode EXPLICIT */
+    const double *root_tris;         /* device f64[H*9] from cbtm_root_triangles */
+    double prm[CBTM_PRM_WORDS];      /* HOST values, LodDecide._prm layout
+                                        (lod.py:286-304), copied by value */
+} cbtm_verdict;
+
+/* ---- sizes ------------------------------------------------------------- */
+int cbtm_abi_version(void);
+/* number of u64 words of the bitfield (>= 16: one 128-byte line) */
+size_t cbtm_bitfield_words(int depth);
+/* number of u32 entries of the counter heap (index 0 unused) */
+size_t cbtm_counter_words(int depth);
+/* scratch bytes needed by cbtm_update / cbtm_sum_reduce for one pool */
+size_t cbtm_workspace_bytes(int depth);
+/* scratch bytes needed by the CBT-only calls (sum_reduce, index, decode) */
+size_t cbtm_cbt_workspace_bytes(int depth);
+
+/* ---- CBT: Cbt.sum_reduce / sum_reduce_array (cbt.py:61-68, 165-170) ------ */
+int cbtm_sum_reduce(const uint64_t *bits, uint32_t *counters, int depth,
+                    void *workspace, size_t workspace_bytes, uintptr_t stream);
+
+/* ---- CBT: one_to_bit_id / zero_to_bit_id and their batch forms
+ *      (cbt.py:75-107, 127-162).  ranks: device i64[K] or NULL for 0..K-1.
+ *      out: device i32[K].  Ranks must be < count (ones) / < N - count (zeros);
+ *      an out-of-range rank yields -1 in `out`. */
+int cbtm_decode_ones(const uint64_t *bits, const uint32_t *counters, int depth,
+                     const int64_t *ranks, int64_t K, int32_t *out, uintptr_t stream);
+int cbtm_decode_zeros(const uint64_t *bits, const uint32_t *counters, int depth,
+                      const int64_t *ranks, int64_t K, int32_t *out, uintptr_t stream);
+
+/* ---- stage 2, k_cache_pointers (kernels.py:244-252) as a stream compaction:
+ *      cache_live[i] = slot of the i-th set bit for i < n; if cache_free is not
+ *      NULL, cache_free[i] = slot of the i-th unset bit for i < N - n.  Entries
+ *      beyond are left untouched.  dispatch (may be NULL) receives the indirect
+ *      dispatch arguments {ceil(n/256), 1, 1, n}. */
+int cbtm_index(const uint64_t *bits, const uint32_t *counters, int depth,
+               int32_t *cache_live, int32_t *cache_free, uint32_t *dispatch,
+               uintptr_t stream);
+
+/* ---- parity views of the reference heap layout (cbt.py:31, Cbt.nodes/leaves) */
+/* leaves: device u32[N] of 0/1 -> packed bitfield (counters are NOT rebuilt) */
+int cbtm_import_leaves(uint64_t *bits, int depth, const uint32_t *leaves, uintptr_t stream);
+/* bitfield + counters -> device u32[2N] heap; every level is written, levels
+ * below the counter heap are recomputed from the bitfield */
+int cbtm_export_nodes(const uint64_t *bits, const uint32_t *counters, int depth,
+                      uint32_t *nodes, uintptr_t stream);
+
+/* ---- initialize (state.py:139-156): fills every pool array with the
+ *      reference's initial values, seeds root bisectors at slots [0, H) and
+ *      rebuilds the counters.  he_*: device i32[H]. */
+int cbtm_initialize(const cbtm_pool *pool, const int32_t *he_next, const int32_t *he_prev,
+                    const int32_t *he_twin, int32_t n_halfedges, uintptr_t stream);
+
+/* ---- root bisector vertices per halfedge (bisector.py:154-173): v0, v1 and
+ *      the face mean accumulated along `next`; out f64[H*9]. */
+int cbtm_root_triangles(const int32_t *he_next, const int32_t *he_vert,
+                        const double *positions, int32_t n_halfedges, double *out,
+                        uintptr_t stream);
+
+/* ---- verdict sources standalone (KernelDecide.fill, pipeline.py:87-119;
+ *      _k_verdict_lod, lod.py:177-269): verdicts[i] for the current cache_live
+ *      order, i < count (count read from the CBT root on device). */
+int cbtm_classify(const cbtm_pool *pool, const cbtm_verdict *verdict, int8_t *verdicts,
+                  uintptr_t stream);
+
+/* ---- triangle export (state.decode_live / nb_decode_tris, bisector.py:186-189):
+ *      out f64[K*9] for ids[K] (device). */
+int cbtm_decode_triangles(const uint64_t *ids, int64_t K, int32_t rank,
+                          const double *root_tris, double *out, uintptr_t stream);
+
+/* ---- ParallelEngine.update (pipeline.py:204-322): one nine-stage frame.
+ *      cbtm_update            = stages 1-9
+ *      cbtm_update_begin      = stages 1-2 (counter reset + cache pointers); after
+ *                               it the caller may read ids[cache_live[:n]] to
+ *                               evaluate host verdicts (python-callable path)
+ *      cbtm_update_finish     = stages 3-9
+ *      Six UpdateStats counters + live counts land in pool->stats (device). */
+int cbtm_update(const cbtm_pool *pool, const cbtm_verdict *verdict, uintptr_t stream);
+int cbtm_update_begin(const cbtm_pool *pool, uintptr_t stream);
+int cbtm_update_finish(const cbtm_pool *pool, const cbtm_verdict *verdict, uintptr_t stream);
+
+/* ---- ParallelEngine.run_epochs / cmd_animate (pipeline.py:324-337,
+ *      cli.py:226-231) for LOD sequences: n_frames updates back to back, no host
+ *      synchronisation; prm_host is HOST f64[n_frames*23]; stats_out (device
+ *      i64[n_frames*CBTM_STATS_WORDS], may be NULL) receives each frame's stats. */
+int cbtm_run_lod_sequence(const cbtm_pool *pool, const double *root_tris,
+                          const double *prm_host, int32_t n_frames, int64_t *stats_out,
+                          uintptr_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CBTM_H_ */

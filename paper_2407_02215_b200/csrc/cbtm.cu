@@ -1,0 +1,325 @@
+// cbtm.cu -- C ABI of libcbtm.so (see include/cbtm.h).  Host-side launch logic
+// only; the kernels live in the .cuh files next to this one.
+//
+// Build (see paper_2407_02215_b200/build.py):
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false
+//        --shared -Xcompiler -fPIC -o libcbtm.so cbtm.cu
+#include "cbtm_frame.cuh"
+
+using namespace cbtm;
+
+namespace {
+
+int g_sm_count = 0;
+
+inline int sm_count()
+{
+    if (g_sm_count == 0) {
+        int dev = 0, n = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+            n = 148; // B200
+        g_sm_count = n;
+    }
+    return g_sm_count;
+}
+
+inline int status(cudaError_t e) { return e == cudaSuccess ? 0 : -(int)e; }
+inline int launch_status() { return status(cudaGetLastError()); }
+inline bool bad_depth(int d) { return d < CBTM_MIN_DEPTH || d > CBTM_MAX_DEPTH; }
+inline cudaStream_t as_stream(uintptr_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// grid for kernels that stride over up to `units` work items of `per_cta` each
+inline unsigned strided_grid(uint64_t units, uint64_t per_cta, int ctas_per_sm)
+{
+    uint64_t want = (units + per_cta - 1) / per_cta;
+    const uint64_t cap = (uint64_t)sm_count() * ctas_per_sm;
+    if (want > cap) want = cap;
+    return want ? (unsigned)want : 1u;
+}
+
+int reduce_launch(const uint64_t *bits, uint32_t *counters, int depth, unsigned *ticket,
+                  int64_t *live_after, cudaStream_t st)
+{
+    const Geo g = make_geo(depth);
+    const unsigned tiles = g.nblocks > (unsigned)RED_TILE_BLOCKS ? g.nblocks / RED_TILE_BLOCKS : 1u;
+    const uint32_t n_vec = (uint32_t)(bitfield_words(depth) / 2);
+    k_sum_reduce<<<tiles, RED_THREADS, 0, st>>>(reinterpret_cast<const uint4 *>(bits), counters, g.lc,
+                                                n_vec, ticket, live_after);
+    return launch_status();
+}
+
+int check_pool(const cbtm_pool *p, bool need_ws)
+{
+    if (!p) return CBTM_E_NULL;
+    if (bad_depth(p->depth)) return CBTM_E_DEPTH;
+    if (!p->ids || !p->nexts || !p->prevs || !p->twins || !p->commands || !p->reserved ||
+        !p->cache_live || !p->cache_free || !p->counter || !p->bits || !p->counters)
+        return CBTM_E_NULL;
+    if (need_ws) {
+        if (!p->workspace) return CBTM_E_NULL;
+        if (p->workspace_bytes < carve_workspace(nullptr, p->depth, nullptr)) return CBTM_E_WORKSPACE;
+    }
+    if (p->rank < 1 || p->rank > 62 || p->max_depth < 0) return CBTM_E_RANGE;
+    return 0;
+}
+
+int fill_args(const cbtm_pool *pool, const cbtm_verdict *v, FrameArgs *a)
+{
+    a->pool = *pool;
+    carve_workspace(pool->workspace, pool->depth, &a->ws);
+    a->use_prm_seq = 0;
+    a->pad_ = 0;
+    a->vexplicit = nullptr;
+    a->root_tris = nullptr;
+    a->vmode = CBTM_VERDICT_CONST;
+    a->vvalue = 0;
+    for (int k = 0; k < CBTM_PRM_WORDS; ++k) a->prm[k] = 0.0;
+    if (!v) return 0;
+    if (v->mode < CBTM_VERDICT_CONST || v->mode > CBTM_VERDICT_EXPLICIT) return CBTM_E_MODE;
+    a->vmode = v->mode;
+    a->vvalue = v->value;
+    if (v->mode == CBTM_VERDICT_CONST && (v->value < 0 || v->value > 2)) return CBTM_E_MODE;
+    if (v->mode == CBTM_VERDICT_EXPLICIT) {
+        if (!v->explicit_verdicts) return CBTM_E_NULL;
+        a->vexplicit = v->explicit_verdicts;
+    }
+    if (v->mode == CBTM_VERDICT_LOD) {
+        if (!v->root_tris) return CBTM_E_NULL;
+        a->root_tris = v->root_tris;
+        for (int k = 0; k < CBTM_PRM_WORDS; ++k) a->prm[k] = v->prm[k];
+    }
+    return 0;
+}
+
+unsigned frame_grid(int depth)
+{
+    return strided_grid((uint64_t)1 << depth, CHUNK, 8);
+}
+
+int index_launch(const cbtm_pool *pool, cudaStream_t st)
+{
+    const Geo g = make_geo(pool->depth);
+    int32_t *freep = (pool->flags & CBTM_POOL_FULL_FREE_CACHE) ? pool->cache_free : nullptr;
+    const unsigned grid = strided_grid(g.nblocks, IDX_WARPS, 6);
+    k_index<<<grid, IDX_WARPS * 32, 0, st>>>(reinterpret_cast<const uint32_t *>(pool->bits),
+                                             pool->counters, pool->depth, pool->cache_live, freep,
+                                             pool->dispatch);
+    return launch_status();
+}
+
+// stages 3-9 for a prepared FrameArgs
+int finish_launch(const FrameArgs &a, int64_t *stats_seq, cudaStream_t st)
+{
+    const unsigned grid = frame_grid(a.pool.depth);
+    k_classify<<<grid, CHUNK, 0, st>>>(a, nullptr);
+    k_admit<<<1, ADMIT_THREADS, 0, st>>>(a);
+    k_scatter<<<grid, CHUNK, 0, st>>>(a);
+    k_agree<<<grid, CHUNK, 0, st>>>(a);
+    k_alloc_scan<<<1, ADMIT_THREADS, 0, st>>>(a);
+    k_reserve<<<grid, CHUNK, 0, st>>>(a);
+    k_apply<<<grid, CHUNK, 0, st>>>(a);
+    int rc = launch_status();
+    if (rc) return rc;
+    rc = reduce_launch(a.pool.bits, a.pool.counters, a.pool.depth, a.ws.ticket, nullptr, st);
+    if (rc) return rc;
+    k_publish<<<1, 32, 0, st>>>(a, stats_seq);
+    return launch_status();
+}
+
+} // namespace
+
+extern "C" {
+
+int cbtm_abi_version(void) { return CBTM_ABI_VERSION; }
+
+size_t cbtm_bitfield_words(int depth) { return bad_depth(depth) ? 0 : bitfield_words(depth); }
+
+size_t cbtm_counter_words(int depth) { return bad_depth(depth) ? 0 : counter_words(depth); }
+
+size_t cbtm_workspace_bytes(int depth)
+{
+    return bad_depth(depth) ? 0 : carve_workspace(nullptr, depth, nullptr);
+}
+
+size_t cbtm_cbt_workspace_bytes(int depth) { return bad_depth(depth) ? 0 : 256; }
+
+int cbtm_sum_reduce(const uint64_t *bits, uint32_t *counters, int depth, void *workspace,
+                    size_t workspace_bytes, uintptr_t stream)
+{
+    if (bad_depth(depth)) return CBTM_E_DEPTH;
+    if (!bits || !counters || !workspace) return CBTM_E_NULL;
+    if (workspace_bytes < 256) return CBTM_E_WORKSPACE;
+    // the ticket is word 0 of the workspace (also of a pool's frame workspace); it
+    // must be zero on entry and the last CTA leaves it zero again
+    return reduce_launch(bits, counters, depth, reinterpret_cast<unsigned *>(workspace), nullptr,
+                         as_stream(stream));
+}
+
+int cbtm_decode_ones(const uint64_t *bits, const uint32_t *counters, int depth, const int64_t *ranks,
+                     int64_t K, int32_t *out, uintptr_t stream)
+{
+    if (bad_depth(depth)) return CBTM_E_DEPTH;
+    if (!bits || !counters || (K > 0 && !out)) return CBTM_E_NULL;
+    if (K < 0) return CBTM_E_RANGE;
+    if (K == 0) return 0;
+    k_decode<true><<<strided_grid((uint64_t)K, 256, 8), 256, 0, as_stream(stream)>>>(bits, counters, depth,
+                                                                                   ranks, K, out);
+    return launch_status();
+}
+
+int cbtm_decode_zeros(const uint64_t *bits, const uint32_t *counters, int depth, const int64_t *ranks,
+                      int64_t K, int32_t *out, uintptr_t stream)
+{
+    if (bad_depth(depth)) return CBTM_E_DEPTH;
+    if (!bits || !counters || (K > 0 && !out)) return CBTM_E_NULL;
+    if (K < 0) return CBTM_E_RANGE;
+    if (K == 0) return 0;
+    k_decode<false><<<strided_grid((uint64_t)K, 256, 8), 256, 0, as_stream(stream)>>>(bits, counters, depth,
+                                                                                    ranks, K, out);
+    return launch_status();
+}
+
+int cbtm_index(const uint64_t *bits, const uint32_t *counters, int depth, int32_t *cache_live,
+               int32_t *cache_free, uint32_t *dispatch, uintptr_t stream)
+{
+    if (bad_depth(depth)) return CBTM_E_DEPTH;
+    if (!bits || !counters || !cache_live) return CBTM_E_NULL;
+    const Geo g = make_geo(depth);
+    k_index<<<strided_grid(g.nblocks, IDX_WARPS, 6), IDX_WARPS * 32, 0, as_stream(stream)>>>(
+        reinterpret_cast<const uint32_t *>(bits), counters, depth, cache_live, cache_free, dispatch);
+    return launch_status();
+}
+
+int cbtm_import_leaves(uint64_t *bits, int depth, const uint32_t *leaves, uintptr_t stream)
+{
+    if (bad_depth(depth)) return CBTM_E_DEPTH;
+    if (!bits || !leaves) return CBTM_E_NULL;
+    k_import_leaves<<<strided_grid(bitfield_words(depth) * 2, 256, 8), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<uint32_t *>(bits), depth, leaves);
+    return launch_status();
+}
+
+int cbtm_export_nodes(const uint64_t *bits, const uint32_t *counters, int depth, uint32_t *nodes,
+                      uintptr_t stream)
+{
+    if (bad_depth(depth)) return CBTM_E_DEPTH;
+    if (!bits || !counters || !nodes) return CBTM_E_NULL;
+    k_export_nodes<<<strided_grid((uint64_t)2 << depth, 256, 8), 256, 0, as_stream(stream)>>>(
+        bits, counters, depth, nodes);
+    return launch_status();
+}
+
+int cbtm_initialize(const cbtm_pool *pool, const int32_t *he_next, const int32_t *he_prev,
+                    const int32_t *he_twin, int32_t n_halfedges, uintptr_t stream)
+{
+    int rc = check_pool(pool, true);
+    if (rc) return rc;
+    if (!he_next || !he_prev || !he_twin) return CBTM_E_NULL;
+    if (n_halfedges < 1 || ((int64_t)n_halfedges > ((int64_t)1 << pool->depth))) return CBTM_E_RANGE;
+    Workspace ws;
+    carve_workspace(pool->workspace, pool->depth, &ws);
+    cudaStream_t st = as_stream(stream);
+    k_initialize<<<strided_grid((uint64_t)1 << pool->depth, 256, 8), 256, 0, st>>>(
+        *pool, he_next, he_prev, he_twin, n_halfedges, ws.ctl, ws.ticket);
+    rc = launch_status();
+    if (rc) return rc;
+    return reduce_launch(pool->bits, pool->counters, pool->depth, ws.ticket, nullptr, st);
+}
+
+int cbtm_root_triangles(const int32_t *he_next, const int32_t *he_vert, const double *positions,
+                        int32_t n_halfedges, double *out, uintptr_t stream)
+{
+    if (!he_next || !he_vert || !positions || !out) return CBTM_E_NULL;
+    if (n_halfedges < 1) return CBTM_E_RANGE;
+    k_root_triangles<<<(n_halfedges + 127) / 128, 128, 0, as_stream(stream)>>>(he_next, he_vert, positions,
+                                                                              n_halfedges, out);
+    return launch_status();
+}
+
+int cbtm_classify(const cbtm_pool *pool, const cbtm_verdict *verdict, int8_t *verdicts, uintptr_t stream)
+{
+    int rc = check_pool(pool, true);
+    if (rc) return rc;
+    if (!verdict || !verdicts) return CBTM_E_NULL;
+    FrameArgs a;
+    rc = fill_args(pool, verdict, &a);
+    if (rc) return rc;
+    k_classify<<<frame_grid(pool->depth), CHUNK, 0, as_stream(stream)>>>(a, verdicts);
+    return launch_status();
+}
+
+int cbtm_decode_triangles(const uint64_t *ids, int64_t K, int32_t rank, const double *root_tris,
+                          double *out, uintptr_t stream)
+{
+    if (!ids || !root_tris || !out) return CBTM_E_NULL;
+    if (K < 0 || rank < 1) return CBTM_E_RANGE;
+    if (K == 0) return 0;
+    k_decode_triangles<<<strided_grid((uint64_t)K, 256, 8), 256, 0, as_stream(stream)>>>(ids, K, rank,
+                                                                                       root_tris, out);
+    return launch_status();
+}
+
+int cbtm_update_begin(const cbtm_pool *pool, uintptr_t stream)
+{
+    const int rc = check_pool(pool, true);
+    if (rc) return rc;
+    return index_launch(pool, as_stream(stream));
+}
+
+int cbtm_update_finish(const cbtm_pool *pool, const cbtm_verdict *verdict, uintptr_t stream)
+{
+    int rc = check_pool(pool, true);
+    if (rc) return rc;
+    if (!verdict) return CBTM_E_NULL;
+    FrameArgs a;
+    rc = fill_args(pool, verdict, &a);
+    if (rc) return rc;
+    return finish_launch(a, nullptr, as_stream(stream));
+}
+
+int cbtm_update(const cbtm_pool *pool, const cbtm_verdict *verdict, uintptr_t stream)
+{
+    const int rc = cbtm_update_begin(pool, stream);
+    if (rc) return rc;
+    return cbtm_update_finish(pool, verdict, stream);
+}
+
+int cbtm_run_lod_sequence(const cbtm_pool *pool, const double *root_tris, const double *prm_host,
+                          int32_t n_frames, int64_t *stats_out, uintptr_t stream)
+{
+    int rc = check_pool(pool, true);
+    if (rc) return rc;
+    if (!root_tris || !prm_host) return CBTM_E_NULL;
+    if (n_frames < 0) return CBTM_E_RANGE;
+    cudaStream_t st = as_stream(stream);
+    cbtm_verdict v;
+    v.mode = CBTM_VERDICT_LOD;
+    v.value = 0;
+    v.explicit_verdicts = nullptr;
+    v.root_tris = root_tris;
+    for (int k = 0; k < CBTM_PRM_WORDS; ++k) v.prm[k] = 0.0;
+    FrameArgs a;
+    rc = fill_args(pool, &v, &a);
+    if (rc) return rc;
+    a.use_prm_seq = 1;
+    for (int32_t done = 0; done < n_frames;) {
+        const int32_t batch = n_frames - done < MAX_SEQ_FRAMES ? n_frames - done : MAX_SEQ_FRAMES;
+        rc = status(cudaMemcpyAsync(a.ws.prm_seq, prm_host + (size_t)CBTM_PRM_WORDS * done,
+                                    sizeof(double) * CBTM_PRM_WORDS * batch, cudaMemcpyHostToDevice, st));
+        if (rc) return rc;
+        rc = status(cudaMemsetAsync(&a.ws.ctl->seq_frame, 0, sizeof(uint32_t), st));
+        if (rc) return rc;
+        int64_t *so = stats_out ? stats_out + (size_t)CBTM_STATS_WORDS * done : nullptr;
+        for (int32_t f = 0; f < batch; ++f) {
+            rc = index_launch(pool, st);
+            if (rc) return rc;
+            rc = finish_launch(a, so, st);
+            if (rc) return rc;
+        }
+        done += batch;
+    }
+    return 0;
+}
+
+} // extern "C"

@@ -1,0 +1,916 @@
+// cbtm_frame.cuh -- the per-frame bisector update (stages 3-8 of
+// ParallelEngine.update, pkg/src/cbtmesh/pipeline.py:204-322) as deterministic
+// data-parallel kernels.
+//
+// The serial reference decides admission and slot placement through two
+// order-dependent atomics (kernels.py:283-288, 315-319, 357-360).  Here both are
+// restated as scans over the live ranks so that the result is bit-identical to
+// the reference at threads=1 no matter how the GPU schedules the work:
+//
+//   admission  accept rank i iff running + need_i <= F, running over accepted
+//              needs in rank order  ==  every rank before the first overflow
+//              i0 is accepted; from i0 on a first-fit walk accepts any later
+//              rank whose need still fits the remaining room (room < 187, so at
+//              most 93 acceptances; k_admit does this in one CTA)
+//   placement  rank i with n_alloc_i slots receives the free ranks
+//              [T - incl_i, T - incl_i + n_alloc_i), incl = inclusive scan of
+//              n_alloc, T = total admitted reservation
+//
+// Launch order per frame (all on one stream, no host synchronisation):
+//   k_classify -> k_admit -> k_scatter -> k_agree -> k_alloc_scan -> k_reserve
+//   -> k_apply -> k_sum_reduce
+#pragma once
+
+#include "cbtm_cbt.cuh"
+#include "cbtm_classify.cuh"
+
+namespace cbtm {
+
+constexpr int TAIL_MAX = 96;
+constexpr int ADMIT_THREADS = 1024;
+constexpr int MAX_SEQ_FRAMES = 4096;
+
+// device-resident control block of one pool (lives in the workspace)
+struct Control {
+    int64_t n, F, T, A; // live, free, reserved total, allocated total
+    int64_t i0;         // first rank rejected by admission (n if none)
+    int32_t tail_count;
+    uint32_t seq_frame; // index into prm_seq for sequence runs
+    int32_t tail_idx[TAIL_MAX];
+    int64_t stats[CBTM_STATS_WORDS];
+};
+
+struct Workspace {
+    uint8_t *need8;   // [N] by live rank: slots to reserve (0 = no command)
+    uint8_t *mbits8;  // [N] by live rank: merge command bits of a merge request
+    uint8_t *nalloc8; // [N] by live rank: slots actually allocated
+    uint8_t *flags8;  // [N] by slot: bit0 = member of an agreed merge
+    uint32_t *chunk_need;
+    uint64_t *chunk_need_off;
+    uint32_t *chunk_alloc;
+    uint64_t *chunk_alloc_off;
+    uint8_t *chunk_minneed;
+    Control *ctl;
+    double *prm_seq;  // [MAX_SEQ_FRAMES * 23]
+    unsigned *ticket; // first word of the workspace: k_sum_reduce's CTA ticket
+};
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Carves the caller's scratch buffer.  Returns the bytes used.
+inline size_t carve_workspace(void *base, int depth, Workspace *ws)
+{
+    const size_t N = (size_t)1 << depth;
+    const size_t nch = (N + CHUNK - 1) / CHUNK;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        void *p = base ? (char *)base + off : nullptr;
+        off = align_up(off + bytes, 256);
+        return p;
+    };
+    Workspace w;
+    w.ticket = (unsigned *)take(256); // must stay first: cbtm_sum_reduce uses word 0
+    w.ctl = (Control *)take(sizeof(Control));
+    w.prm_seq = (double *)take(sizeof(double) * CBTM_PRM_WORDS * MAX_SEQ_FRAMES);
+    w.need8 = (uint8_t *)take(N);
+    w.mbits8 = (uint8_t *)take(N);
+    w.nalloc8 = (uint8_t *)take(N);
+    w.flags8 = (uint8_t *)take(N);
+    w.chunk_need = (uint32_t *)take(4 * nch);
+    w.chunk_need_off = (uint64_t *)take(8 * nch);
+    w.chunk_alloc = (uint32_t *)take(4 * nch);
+    w.chunk_alloc_off = (uint64_t *)take(8 * nch);
+    w.chunk_minneed = (uint8_t *)take(nch);
+    if (ws) *ws = w;
+    return off;
+}
+
+struct FrameArgs {
+    cbtm_pool pool;
+    Workspace ws;
+    int32_t vmode, vvalue;
+    const int8_t *vexplicit;
+    const double *root_tris;
+    int32_t use_prm_seq;
+    int32_t pad_;
+    double prm[CBTM_PRM_WORDS];
+};
+
+// ---------------------------------------------------------------------------
+// merge configuration (kernels.py:112-191)
+// ---------------------------------------------------------------------------
+struct MergeCfg {
+    int kind; // 0 none, 1 boundary pair, 2 quad
+    int32_t sib, oth, j4;
+};
+
+__device__ __forceinline__ MergeCfg merge_config(const cbtm_pool &p, int32_t s, uint64_t j1)
+{
+    MergeCfg c = {0, -1, -1, -1};
+    if (depth_of(j1, p.rank) < 1) return c; // roots never merge
+    const bool odd = j1 & 1;
+    const int32_t nx = p.nexts[s], pv = p.prevs[s];
+    const int32_t sib = odd ? pv : nx;
+    const int32_t oth = odd ? nx : pv;
+    if (sib < 0 || (p.ids[sib] >> 1) != (j1 >> 1)) return c;
+    if (oth < 0) {
+        c.kind = 1;
+        c.sib = sib;
+        return c;
+    }
+    const uint64_t jo = p.ids[oth];
+    if (bit_length64(jo) != bit_length64(j1)) return c;
+    const int32_t j4 = odd ? p.nexts[oth] : p.prevs[oth];
+    if (j4 < 0 || (p.ids[j4] >> 1) != (jo >> 1)) return c;
+    c.kind = 2;
+    c.sib = sib;
+    c.oth = oth;
+    c.j4 = j4;
+    return c;
+}
+
+__device__ __forceinline__ bool wants_only_merge(uint32_t cmd)
+{
+    return !(cmd & CBTM_CMD_SPLIT_MASK) && (cmd & CBTM_CMD_MERGE);
+}
+
+// reserved slot of the parent that replaces merging member m (kernels.py:159-180)
+__device__ __forceinline__ int32_t merge_parent_slot(const cbtm_pool &p, int32_t m)
+{
+    const uint64_t jm = p.ids[m];
+    const MergeCfg c = merge_config(p, m, jm);
+    int32_t owner = m;
+    uint64_t best = jm;
+    const uint64_t js = p.ids[c.sib];
+    if (js < best) {
+        best = js;
+        owner = c.sib;
+    }
+    if (c.kind == 2) {
+        const uint64_t jo = p.ids[c.oth], j4 = p.ids[c.j4];
+        if (jo < best) {
+            best = jo;
+            owner = c.oth;
+        }
+        if (j4 < best) {
+            best = j4;
+            owner = c.j4;
+        }
+    }
+    if (c.kind == 1 || (jm >> 1) == (best >> 1)) return p.reserved[4 * (size_t)owner];
+    return p.reserved[4 * (size_t)owner + 1];
+}
+
+// ---------------------------------------------------------------------------
+// stage 3 + 4a: reset commands, evaluate verdicts, compute each rank's
+// reservation need (3d+4 for a split, 2 for a valid merge, 0 otherwise).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(CHUNK)
+k_classify(const __grid_constant__ FrameArgs a, int8_t *__restrict__ verdict_out)
+{
+    __shared__ double prm[CBTM_PRM_WORDS];
+    __shared__ uint32_t wsum[CHUNK / 32], wmin[CHUNK / 32];
+    const cbtm_pool &p = a.pool;
+    const uint32_t n = p.counters[1];
+    const uint32_t nch = (n + CHUNK - 1) / CHUNK;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    if (a.vmode == CBTM_VERDICT_LOD) {
+        if (tid < CBTM_PRM_WORDS)
+            prm[tid] = a.use_prm_seq ? a.ws.prm_seq[(size_t)CBTM_PRM_WORDS * a.ws.ctl->seq_frame + tid]
+                                     : a.prm[tid];
+        __syncthreads();
+    }
+
+    for (uint32_t chunk = blockIdx.x; chunk < nch; chunk += gridDim.x) {
+        const uint32_t i = chunk * CHUNK + tid;
+        uint32_t need = 0, mbits = 0;
+        if (i < n) {
+            const int32_t s = p.cache_live[i];
+            const uint64_t id = p.ids[s];
+            int v;
+            switch (a.vmode) {
+            case CBTM_VERDICT_CONST: v = a.vvalue; break;
+            case CBTM_VERDICT_UNIFORM: v = depth_of(id, p.rank) < a.vvalue ? 1 : 0; break;
+            case CBTM_VERDICT_LOD: v = lod_verdict(id, p.rank, p.max_depth, a.root_tris, prm); break;
+            default: v = a.vexplicit[i]; break;
+            }
+            if (verdict_out) {
+                verdict_out[i] = (int8_t)v; // standalone verdict evaluation: no side effects
+            } else {
+                p.commands[s] = 0; // stage 3
+                if (v == 1) {
+                    const int d = depth_of(id, p.rank);
+                    if (d < p.max_depth) need = 3 * d + 4;
+                } else if (v == 2) {
+                    const MergeCfg c = merge_config(p, s, id);
+                    if (c.kind) {
+                        need = 2;
+                        mbits = CBTM_CMD_MERGE;
+                        uint64_t lowest = umin64(id, p.ids[c.sib]);
+                        if (c.kind == 2) {
+                            mbits |= CBTM_CMD_QUAD;
+                            lowest = umin64(lowest, p.ids[c.oth]);
+                            lowest = umin64(lowest, p.ids[c.j4]);
+                        }
+                        if (lowest == id) mbits |= CBTM_CMD_OWNER;
+                    }
+                }
+                a.ws.need8[i] = (uint8_t)need;
+                a.ws.mbits8[i] = (uint8_t)mbits;
+            }
+        }
+        if (verdict_out) continue;
+        uint32_t sum = warp_sum(need);
+        uint32_t mn = need ? need : 255u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(FULL_MASK, mn, o));
+        if (lane == 0) {
+            wsum[warp] = sum;
+            wmin[warp] = mn;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t ts = 0, tm = 255u;
+#pragma unroll
+            for (int w = 0; w < CHUNK / 32; ++w) {
+                ts += wsum[w];
+                tm = min(tm, wmin[w]);
+            }
+            a.ws.chunk_need[chunk] = ts;
+            a.ws.chunk_minneed[chunk] = (uint8_t)tm;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// stage 4b (one CTA): admission.  Scans the per-chunk needs, locates the first
+// overflowing rank i0 and runs the first-fit tail walk.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(ADMIT_THREADS)
+k_admit(const __grid_constant__ FrameArgs a)
+{
+    __shared__ uint32_t scratch[32];
+    __shared__ uint32_t s_warpmin[32];
+    __shared__ unsigned long long s_carry;
+    __shared__ uint32_t s_c0, s_found, s_next, s_room;
+    __shared__ long long s_pos;
+    __shared__ int s_cnt;
+
+    const cbtm_pool &p = a.pool;
+    Control *ctl = a.ws.ctl;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t n = p.counters[1];
+    const uint64_t F = ((uint64_t)1 << p.depth) - n;
+    const uint32_t nch = (n + CHUNK - 1) / CHUNK;
+
+    if (tid < CBTM_STATS_WORDS && tid != CBTM_STAT_FRAME) ctl->stats[tid] = 0;
+    if (tid == 0) {
+        s_carry = 0;
+        s_c0 = nch;
+    }
+    __syncthreads();
+
+    // ---- exclusive scan of the chunk needs, first overflowing chunk ----
+    for (uint32_t base = 0; base < nch; base += ADMIT_THREADS) {
+        const uint32_t c = base + tid;
+        const uint32_t v = c < nch ? a.ws.chunk_need[c] : 0;
+        uint32_t total;
+        const uint32_t incl = block_inclusive_scan<ADMIT_THREADS>(v, scratch, &total);
+        const unsigned long long carry = s_carry;
+        if (c < nch) {
+            const unsigned long long off = carry + incl - v;
+            a.ws.chunk_need_off[c] = off;
+            if (off + v > F) atomicMin(&s_c0, c);
+        }
+        __syncthreads();
+        if (tid == 0) s_carry = carry + total;
+        __syncthreads();
+    }
+    const unsigned long long total_need = s_carry;
+    const uint32_t c0 = s_c0;
+
+    if (c0 == nch) { // everything fits
+        if (tid == 0) {
+            ctl->n = n;
+            ctl->F = (int64_t)F;
+            ctl->T = (int64_t)total_need;
+            ctl->i0 = n;
+            ctl->tail_count = 0;
+            ctl->stats[CBTM_STAT_LIVE_BEFORE] = n;
+            ctl->stats[CBTM_STAT_RESERVED] = (int64_t)total_need;
+        }
+        return;
+    }
+
+    // ---- first overflowing rank inside chunk c0 ----
+    {
+        const uint32_t i = c0 * CHUNK + tid;
+        const uint32_t v = (tid < CHUNK && i < n) ? a.ws.need8[i] : 0;
+        uint32_t total;
+        const uint32_t incl = block_inclusive_scan<ADMIT_THREADS>(v, scratch, &total);
+        const unsigned long long off = a.ws.chunk_need_off[c0];
+        if (tid == 0) s_found = 0xffffffffu;
+        __syncthreads();
+        if (tid < CHUNK && v && off + incl > F) atomicMin(&s_found, (uint32_t)tid);
+        __syncthreads();
+        const uint32_t f = s_found; // exists by construction
+        if ((uint32_t)tid == f) {
+            s_room = (uint32_t)(F - (off + incl - v));
+            s_pos = (long long)c0 * CHUNK + f;
+            ctl->i0 = (long long)c0 * CHUNK + f;
+            s_cnt = 0;
+        }
+        __syncthreads();
+    }
+
+    // ---- first-fit tail walk from i0 ----
+    while (true) {
+        const long long pos = s_pos;
+        if (s_room < 2 || pos >= (long long)n) break;
+        const uint32_t c = (uint32_t)(pos / CHUNK);
+        const long long idx = (long long)c * CHUNK + tid;
+        uint32_t need = (tid < CHUNK && idx >= pos && idx < (long long)n) ? a.ws.need8[idx] : 0;
+        while (true) { // accept, in rank order, whatever still fits in this chunk
+            const uint32_t room = s_room;
+            const bool ok = need > 0 && need <= room;
+            const unsigned b = __ballot_sync(FULL_MASK, ok);
+            if (lane == 0) s_warpmin[warp] = b ? (uint32_t)(warp * 32 + __ffs(b) - 1) : 0xffffffffu;
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t m = 0xffffffffu;
+                for (int w = 0; w < CHUNK / 32; ++w) m = min(m, s_warpmin[w]);
+                s_found = m;
+            }
+            __syncthreads();
+            const uint32_t f = s_found;
+            if (f == 0xffffffffu) break;
+            if ((uint32_t)tid == f) {
+                ctl->tail_idx[s_cnt] = (int32_t)idx;
+                s_cnt = s_cnt + 1;
+                s_room = room - need;
+            }
+            if ((uint32_t)tid <= f) need = 0;
+            __syncthreads();
+        }
+        // next chunk holding a need that still fits
+        const uint32_t room = s_room;
+        if (room < 2) break;
+        if (tid == 0) s_next = nch;
+        __syncthreads();
+        for (uint32_t base = c + 1; base < nch; base += ADMIT_THREADS) {
+            const uint32_t cc = base + tid;
+            const bool ok = cc < nch && a.ws.chunk_minneed[cc] <= room;
+            const unsigned b = __ballot_sync(FULL_MASK, ok);
+            if (lane == 0) s_warpmin[warp] = b ? (uint32_t)(base + warp * 32 + __ffs(b) - 1) : 0xffffffffu;
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t m = 0xffffffffu;
+                for (int w = 0; w < ADMIT_THREADS / 32; ++w) m = min(m, s_warpmin[w]);
+                if (m != 0xffffffffu) s_next = m;
+            }
+            __syncthreads();
+            if (s_next != nch) break;
+        }
+        const uint32_t nxt = s_next;
+        __syncthreads();
+        if (nxt >= nch) break;
+        if (tid == 0) s_pos = (long long)nxt * CHUNK;
+        __syncthreads();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int64_t T = (int64_t)F - (int64_t)s_room;
+        ctl->n = n;
+        ctl->F = (int64_t)F;
+        ctl->T = T;
+        ctl->tail_count = s_cnt;
+        ctl->stats[CBTM_STAT_LIVE_BEFORE] = n;
+        ctl->stats[CBTM_STAT_RESERVED] = T;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// stage 4c: scatter the admitted commands.  Splits walk their compatibility
+// chain OR-ing edge-split bits (kernels.py:289-310); merges OR their
+// configuration bits (kernels.py:320-333).  OR is commutative, so the final
+// command words do not depend on scheduling.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void walk_split_chain(const cbtm_pool &p, int32_t s)
+{
+    int32_t cur = s;
+    for (int hops = 0;;) {
+        const uint32_t before = atomicOr(&p.commands[cur], CBTM_CMD_SPLIT_T);
+        if (before & CBTM_CMD_SPLIT_T) break; // another walker owns the rest of the chain
+        const int32_t t = p.twins[cur];
+        if (t < 0) break;
+        if (p.twins[t] == cur) {
+            atomicOr(&p.commands[t], CBTM_CMD_SPLIT_T);
+            break;
+        }
+        if (p.nexts[t] == cur)
+            atomicOr(&p.commands[t], CBTM_CMD_SPLIT_N);
+        else if (p.prevs[t] == cur)
+            atomicOr(&p.commands[t], CBTM_CMD_SPLIT_P);
+        else
+            break;
+        cur = t;
+        if (++hops > 70) break;
+    }
+}
+
+__global__ void __launch_bounds__(CHUNK)
+k_scatter(const __grid_constant__ FrameArgs a)
+{
+    __shared__ int32_t tail[TAIL_MAX];
+    __shared__ uint32_t oom[2];
+    const cbtm_pool &p = a.pool;
+    const Control *ctl = a.ws.ctl;
+    const int tid = threadIdx.x;
+    const uint32_t n = (uint32_t)ctl->n;
+    const uint32_t nch = (n + CHUNK - 1) / CHUNK;
+    const long long i0 = ctl->i0;
+    const int tail_count = ctl->tail_count;
+    if (tid < TAIL_MAX) tail[tid] = tid < tail_count ? ctl->tail_idx[tid] : -1;
+    if (tid < 2) oom[tid] = 0;
+    __syncthreads();
+
+    uint32_t my_oom_s = 0, my_oom_m = 0;
+    for (uint32_t chunk = blockIdx.x; chunk < nch; chunk += gridDim.x) {
+        const uint32_t i = chunk * CHUNK + tid;
+        if (i >= n) continue;
+        const uint32_t need = a.ws.need8[i];
+        if (!need) continue;
+        bool accepted = (long long)i < i0;
+        if (!accepted) {
+            for (int k = 0; k < tail_count; ++k)
+                if (tail[k] == (int32_t)i) accepted = true;
+        }
+        if (!accepted) {
+            if (need == 2) ++my_oom_m; else ++my_oom_s;
+            continue;
+        }
+        const int32_t s = p.cache_live[i];
+        if (need == 2)
+            atomicOr(&p.commands[s], (uint32_t)a.ws.mbits8[i]);
+        else
+            walk_split_chain(p, s);
+    }
+    if (i0 < (long long)n) { // only frames under reservation pressure count rejections
+        if (my_oom_s) atomicAdd(&oom[0], my_oom_s);
+        if (my_oom_m) atomicAdd(&oom[1], my_oom_m);
+        __syncthreads();
+        if (tid < 2 && oom[tid])
+            atomicAdd((unsigned long long *)&a.ws.ctl->stats[tid], (unsigned long long)oom[tid]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// stage 5a: with all commands final, snapshot the merge agreement of every
+// live slot (flags8) and count each rank's allocations (kernels.py:347-368).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(CHUNK)
+k_agree(const __grid_constant__ FrameArgs a)
+{
+    __shared__ uint32_t wsum[CHUNK / 32];
+    const cbtm_pool &p = a.pool;
+    const uint32_t n = (uint32_t)a.ws.ctl->n;
+    const uint32_t nch = (n + CHUNK - 1) / CHUNK;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (uint32_t chunk = blockIdx.x; chunk < nch; chunk += gridDim.x) {
+        const uint32_t i = chunk * CHUNK + tid;
+        uint32_t na = 0;
+        if (i < n) {
+            const int32_t s = p.cache_live[i];
+            const uint32_t cmd = p.commands[s];
+            const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
+            uint32_t agreed = 0;
+            if (sm) {
+                na = 2 + ((sm >> 1) & 1) + ((sm >> 2) & 1);
+            } else if (cmd & CBTM_CMD_MERGE) {
+                const MergeCfg c = merge_config(p, s, p.ids[s]);
+                if (c.kind) {
+                    agreed = wants_only_merge(p.commands[c.sib]);
+                    if (agreed && c.kind == 2)
+                        agreed = wants_only_merge(p.commands[c.oth]) && wants_only_merge(p.commands[c.j4]);
+                }
+                if (agreed && (cmd & CBTM_CMD_OWNER)) na = (cmd & CBTM_CMD_QUAD) ? 2 : 1;
+            }
+            a.ws.flags8[s] = (uint8_t)agreed;
+            a.ws.nalloc8[i] = (uint8_t)na;
+        }
+        const uint32_t sum = warp_sum(na);
+        if (lane == 0) wsum[warp] = sum;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t ts = 0;
+#pragma unroll
+            for (int w = 0; w < CHUNK / 32; ++w) ts += wsum[w];
+            a.ws.chunk_alloc[chunk] = ts;
+        }
+        __syncthreads();
+    }
+}
+
+// stage 5b (one CTA): exclusive scan of the per-chunk allocation counts
+__global__ void __launch_bounds__(ADMIT_THREADS)
+k_alloc_scan(const __grid_constant__ FrameArgs a)
+{
+    __shared__ uint32_t scratch[32];
+    __shared__ unsigned long long s_carry;
+    Control *ctl = a.ws.ctl;
+    const int tid = threadIdx.x;
+    const uint32_t n = (uint32_t)ctl->n;
+    const uint32_t nch = (n + CHUNK - 1) / CHUNK;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < nch; base += ADMIT_THREADS) {
+        const uint32_t c = base + tid;
+        const uint32_t v = c < nch ? a.ws.chunk_alloc[c] : 0;
+        uint32_t total;
+        const uint32_t incl = block_inclusive_scan<ADMIT_THREADS>(v, scratch, &total);
+        const unsigned long long carry = s_carry;
+        if (c < nch) a.ws.chunk_alloc_off[c] = carry + incl - v;
+        __syncthreads();
+        if (tid == 0) s_carry = carry + total;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const int64_t A = (int64_t)s_carry;
+        ctl->A = A;
+        ctl->stats[CBTM_STAT_ALLOCATED] = A;
+        a.pool.counter[0] = ctl->T - A; // reservation slack left in the counter (kernels.py:357)
+    }
+}
+
+// ---------------------------------------------------------------------------
+// stage 5c: hand out free slots.  Rank i owns free ranks [T - incl_i, ...):
+// windows are popped from the top of the reserved range exactly like the serial
+// atomic_sub of kernels.py:357-360.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(CHUNK)
+k_reserve(const __grid_constant__ FrameArgs a)
+{
+    __shared__ uint32_t scratch[32];
+    const cbtm_pool &p = a.pool;
+    const Control *ctl = a.ws.ctl;
+    const Geo g = make_geo(p.depth);
+    const uint32_t n = (uint32_t)ctl->n;
+    const uint32_t nch = (n + CHUNK - 1) / CHUNK;
+    const long long T = ctl->T;
+    const bool full = p.flags & CBTM_POOL_FULL_FREE_CACHE;
+    const int tid = threadIdx.x;
+    for (uint32_t chunk = blockIdx.x; chunk < nch; chunk += gridDim.x) {
+        if (a.ws.chunk_alloc[chunk] == 0) continue;
+        const uint32_t i = chunk * CHUNK + tid;
+        const uint32_t na = i < n ? a.ws.nalloc8[i] : 0;
+        uint32_t total;
+        const uint32_t incl = block_inclusive_scan<CHUNK>(na, scratch, &total);
+        if (!na) continue;
+        const int32_t s = p.cache_live[i];
+        const long long base = T - (long long)(a.ws.chunk_alloc_off[chunk] + incl);
+        for (uint32_t k = 0; k < na; ++k) {
+            const long long r = base + k;
+            int32_t slot;
+            if (full) {
+                slot = p.cache_free[r];
+            } else {
+                slot = cbt_find<false>(p.bits, p.counters, g, (uint32_t)r);
+                p.cache_free[r] = slot;
+            }
+            p.reserved[4 * (size_t)s + k] = slot;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// stages 6 + 7 + 8 fused: write the fresh records, redirect surviving
+// neighbours, flip the occupancy bits.
+//
+// Why fusing is safe: fresh records go to slots that were free at frame start
+// and are read by nobody this frame; redirects touch only pointer fields of
+// *surviving* records, one writer per field (kernels.py:533-594); everything a
+// fill or a redirect reads is either a consumed record (never rewritten), a
+// command word (final since k_scatter), a reservation (final since k_reserve)
+// or the agreement snapshot flags8 (final since k_agree).
+// ---------------------------------------------------------------------------
+enum { E_TWIN = 0, E_NEXT = 1, E_PREV = 2 };
+enum { H_WHOLE = 0, H_V0 = 1, H_V1 = 2, H_V2 = 3 };
+
+// PIECE_IDX of kernels.py:50-72 derived from the child layout: the v0-side half
+// of a split bisector yields [2j] or [4j, 4j+1], the v1-side half follows with
+// [2j+1] or [4j+2, 4j+3].
+__device__ __forceinline__ int piece_index(uint32_t mask, int edge, int half)
+{
+    const int left_n = (mask & CBTM_CMD_SPLIT_P) ? 2 : 1;
+    const int right_n = (mask & CBTM_CMD_SPLIT_N) ? 2 : 1;
+    const int last = left_n + right_n - 1;
+    if (edge == E_TWIN) return half == H_V0 ? 0 : (half == H_V1 ? last : -1);
+    if (edge == E_NEXT) {
+        if (right_n == 1) return half == H_WHOLE ? left_n : -1;
+        return half == H_V1 ? last : (half == H_V2 ? left_n : -1);
+    }
+    if (left_n == 1) return half == H_WHOLE ? 0 : -1;
+    return half == H_V0 ? 0 : (half == H_V2 ? 1 : -1);
+}
+
+// (my edge, my half) seen from the neighbour answering through t_role
+// (kernels.py:75-100; vertex correspondences of state.py:271-279)
+__device__ __forceinline__ void correspond(int my_side, int my_half, int t_role, int &t_edge, int &t_half)
+{
+    if (my_side == E_TWIN) {
+        t_edge = t_role;
+        if (t_role == E_TWIN) t_half = my_half == H_V1 ? H_V0 : H_V1;
+        else if (t_role == E_PREV) t_half = my_half == H_V0 ? H_V2 : H_V0;
+        else t_half = my_half == H_V0 ? H_V1 : H_V2;
+    } else if (my_side == E_NEXT) {
+        if (t_role == E_PREV) {
+            t_edge = E_PREV;
+            t_half = my_half == H_WHOLE ? H_WHOLE : (my_half == H_V1 ? H_V0 : H_V2);
+        } else {
+            t_edge = E_TWIN;
+            t_half = my_half == H_V1 ? H_V0 : H_V1;
+        }
+    } else {
+        if (t_role == E_NEXT) {
+            t_edge = E_NEXT;
+            t_half = my_half == H_WHOLE ? H_WHOLE : (my_half == H_V0 ? H_V1 : H_V2);
+        } else {
+            t_edge = E_TWIN;
+            t_half = my_half == H_V0 ? H_V1 : H_V0;
+        }
+    }
+}
+
+struct ApplyCtx {
+    const cbtm_pool &p;
+    const uint8_t *flags8;
+    uint32_t poison;
+};
+
+// post-update slot of the record across (my_side, my_half); kernels.py:194-238
+__device__ __forceinline__ int32_t piece_of(ApplyCtx &cx, int32_t target, int my_side, int my_half,
+                                            int32_t backref)
+{
+    if (target < 0) return -1;
+    const cbtm_pool &p = cx.p;
+    const uint32_t cmd = p.commands[target];
+    const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
+    if (sm) {
+        int role = -1;
+        if (my_side == E_TWIN) {
+            if (p.twins[target] == backref) role = E_TWIN;
+            else if (p.nexts[target] == backref) role = E_NEXT;
+            else if (p.prevs[target] == backref) role = E_PREV;
+        } else if (my_side == E_NEXT) {
+            if (p.prevs[target] == backref) role = E_PREV;
+            else if (p.twins[target] == backref) role = E_TWIN;
+        } else {
+            if (p.nexts[target] == backref) role = E_NEXT;
+            else if (p.twins[target] == backref) role = E_TWIN;
+        }
+        int idx = -1;
+        if (role >= 0) {
+            int t_edge, t_half;
+            correspond(my_side, my_half, role, t_edge, t_half);
+            idx = piece_index(sm, t_edge, t_half);
+        }
+        if (idx < 0) {
+            ++cx.poison;
+            return -2;
+        }
+        return p.reserved[4 * (size_t)target + idx];
+    }
+    if ((cmd & CBTM_CMD_MERGE) && (cx.flags8[target] & 1)) return merge_parent_slot(p, target);
+    return target;
+}
+
+__device__ __forceinline__ bool survives(const ApplyCtx &cx, int32_t x)
+{
+    const uint32_t cmd = cx.p.commands[x];
+    if (cmd & CBTM_CMD_SPLIT_MASK) return false;
+    return !((cmd & CBTM_CMD_MERGE) && (cx.flags8[x] & 1));
+}
+
+// kernels.py:514-530
+__device__ __forceinline__ void redirect_to(const cbtm_pool &p, int32_t target, int32_t old_slot,
+                                            int32_t new_slot, int first)
+{
+    int32_t *primary = first == E_PREV ? p.prevs : p.nexts;
+    if (primary[target] == old_slot) {
+        primary[target] = new_slot;
+        return;
+    }
+    if (p.twins[target] == old_slot) p.twins[target] = new_slot;
+}
+
+__device__ __forceinline__ void set_live(uint32_t *bits32, int32_t slot)
+{
+    atomicOr(&bits32[slot >> 5], 1u << (slot & 31));
+}
+
+__device__ __forceinline__ void set_free(uint32_t *bits32, int32_t slot)
+{
+    atomicAnd(&bits32[slot >> 5], ~(1u << (slot & 31)));
+}
+
+// kernels.py:373-461 restated over the two halves of the bisector
+__device__ __forceinline__ void apply_split(ApplyCtx &cx, int32_t s, uint32_t sm)
+{
+    const cbtm_pool &p = cx.p;
+    const uint64_t j = p.ids[s];
+    const int32_t nb_n = p.nexts[s], nb_p = p.prevs[s], nb_t = p.twins[s];
+    const int4 r4 = *reinterpret_cast<const int4 *>(p.reserved + 4 * (size_t)s);
+    const int32_t r[4] = {r4.x, r4.y, r4.z, r4.w};
+    const int left_n = (sm & CBTM_CMD_SPLIT_P) ? 2 : 1;
+    const int right_n = (sm & CBTM_CMD_SPLIT_N) ? 2 : 1;
+    const int32_t left_last = r[left_n - 1];
+    const int32_t right_first = r[left_n];
+
+    // stage 6: fresh records
+    if (left_n == 1) {
+        const int32_t a = r[0];
+        p.ids[a] = j << 1;
+        p.nexts[a] = right_first;
+        p.prevs[a] = piece_of(cx, nb_t, E_TWIN, H_V0, s);
+        p.twins[a] = piece_of(cx, nb_p, E_PREV, H_WHOLE, s);
+    } else {
+        const int32_t a = r[0], b = r[1];
+        p.ids[a] = j << 2;
+        p.twins[a] = piece_of(cx, nb_t, E_TWIN, H_V0, s);
+        p.nexts[a] = b;
+        p.prevs[a] = piece_of(cx, nb_p, E_PREV, H_V0, s);
+        p.ids[b] = (j << 2) + 1;
+        p.twins[b] = right_first;
+        p.prevs[b] = a;
+        p.nexts[b] = piece_of(cx, nb_p, E_PREV, H_V2, s);
+    }
+    if (right_n == 1) {
+        const int32_t c = r[left_n];
+        p.ids[c] = (j << 1) + 1;
+        p.prevs[c] = left_last;
+        p.nexts[c] = piece_of(cx, nb_t, E_TWIN, H_V1, s);
+        p.twins[c] = piece_of(cx, nb_n, E_NEXT, H_WHOLE, s);
+    } else {
+        const int32_t c = r[left_n], d = r[left_n + 1];
+        p.ids[c] = (j << 2) + 2;
+        p.twins[c] = left_last;
+        p.nexts[c] = d;
+        p.prevs[c] = piece_of(cx, nb_n, E_NEXT, H_V2, s);
+        p.ids[d] = (j << 2) + 3;
+        p.prevs[d] = c;
+        p.twins[d] = piece_of(cx, nb_t, E_TWIN, H_V1, s);
+        p.nexts[d] = piece_of(cx, nb_n, E_NEXT, H_V1, s);
+    }
+
+    // stage 7: surviving neighbours across unsplit edges (kernels.py:547-561)
+    if (right_n == 1 && nb_n >= 0 && survives(cx, nb_n))
+        redirect_to(p, nb_n, s, r[left_n], E_PREV);
+    if (left_n == 1 && nb_p >= 0 && survives(cx, nb_p))
+        redirect_to(p, nb_p, s, r[0], E_NEXT);
+
+    // stage 8
+    uint32_t *bits32 = reinterpret_cast<uint32_t *>(p.bits);
+    set_free(bits32, s);
+    for (int k = 0; k < left_n + right_n; ++k) set_live(bits32, r[k]);
+}
+
+// one sibling pair (even id e, odd id o) collapses into parent slot par
+__device__ __forceinline__ void apply_merged_pair(ApplyCtx &cx, int32_t e, int32_t o, int32_t par,
+                                                  int32_t twin_slot)
+{
+    const cbtm_pool &p = cx.p;
+    const int32_t n_ext = p.twins[o], q_ext = p.twins[e];
+    p.ids[par] = p.ids[e] >> 1;
+    p.nexts[par] = piece_of(cx, n_ext, E_NEXT, H_WHOLE, o);
+    p.prevs[par] = piece_of(cx, q_ext, E_PREV, H_WHOLE, e);
+    p.twins[par] = twin_slot;
+    if (n_ext >= 0 && survives(cx, n_ext)) redirect_to(p, n_ext, o, par, E_PREV);
+    if (q_ext >= 0 && survives(cx, q_ext)) redirect_to(p, q_ext, e, par, E_NEXT);
+}
+
+__global__ void __launch_bounds__(CHUNK)
+k_apply(const __grid_constant__ FrameArgs a)
+{
+    __shared__ uint32_t acc[5];
+    const cbtm_pool &p = a.pool;
+    const uint32_t n = (uint32_t)a.ws.ctl->n;
+    const uint32_t nch = (n + CHUNK - 1) / CHUNK;
+    const int tid = threadIdx.x;
+    if (tid < 5) acc[tid] = 0;
+    __syncthreads();
+    ApplyCtx cx{p, a.ws.flags8, 0};
+    uint32_t split_freed = 0, merge_freed = 0, split_alloc = 0, merge_alloc = 0;
+    uint32_t *bits32 = reinterpret_cast<uint32_t *>(p.bits);
+
+    for (uint32_t chunk = blockIdx.x; chunk < nch; chunk += gridDim.x) {
+        const uint32_t i = chunk * CHUNK + tid;
+        if (i >= n) continue;
+        const int32_t s = p.cache_live[i];
+        const uint32_t cmd = p.commands[s];
+        const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
+        if (sm) {
+            apply_split(cx, s, sm);
+            ++split_freed;
+            split_alloc += 2 + ((sm >> 1) & 1) + ((sm >> 2) & 1);
+        } else if ((cmd & CBTM_CMD_MERGE) && (a.ws.flags8[s] & 1)) {
+            set_free(bits32, s);
+            ++merge_freed;
+            if (cmd & CBTM_CMD_OWNER) { // kernels.py:464-491, 562-594, 624-628
+                const uint64_t js = p.ids[s];
+                const MergeCfg c = merge_config(p, s, js);
+                const bool s_even = !(js & 1);
+                const int32_t p1 = p.reserved[4 * (size_t)s];
+                if (c.kind == 2) {
+                    const int32_t p2 = p.reserved[4 * (size_t)s + 1];
+                    const bool oth_even = !(p.ids[c.oth] & 1);
+                    apply_merged_pair(cx, s_even ? s : c.sib, s_even ? c.sib : s, p1, p2);
+                    apply_merged_pair(cx, oth_even ? c.oth : c.j4, oth_even ? c.j4 : c.oth, p2, p1);
+                    set_live(bits32, p1);
+                    set_live(bits32, p2);
+                    merge_alloc += 2;
+                } else {
+                    apply_merged_pair(cx, s_even ? s : c.sib, s_even ? c.sib : s, p1, -1);
+                    set_live(bits32, p1);
+                    merge_alloc += 1;
+                }
+            }
+        }
+    }
+    if (split_freed) atomicAdd(&acc[0], split_freed);
+    if (merge_freed) atomicAdd(&acc[1], merge_freed);
+    if (split_alloc) atomicAdd(&acc[2], split_alloc);
+    if (merge_alloc) atomicAdd(&acc[3], merge_alloc);
+    if (cx.poison) atomicAdd(&acc[4], cx.poison);
+    __syncthreads();
+    if (tid < 5 && acc[tid]) {
+        const int slot = tid < 4 ? CBTM_STAT_SPLIT_FREED + tid : CBTM_STAT_POISON;
+        atomicAdd((unsigned long long *)&a.ws.ctl->stats[slot], (unsigned long long)acc[tid]);
+    }
+}
+
+// end of frame: publish the stats block, advance the sequence frame counter
+__global__ void k_publish(const __grid_constant__ FrameArgs a, int64_t *__restrict__ stats_seq)
+{
+    Control *ctl = a.ws.ctl;
+    const int tid = threadIdx.x;
+    if (tid < CBTM_STATS_WORDS) {
+        int64_t v = ctl->stats[tid];
+        if (tid == CBTM_STAT_LIVE_AFTER) v = a.pool.counters[1];
+        if (tid == CBTM_STAT_FRAME) v += 1;
+        if (a.pool.stats) a.pool.stats[tid] = v;
+        if (stats_seq) stats_seq[(size_t)CBTM_STATS_WORDS * ctl->seq_frame + tid] = v;
+        if (tid == CBTM_STAT_FRAME) ctl->stats[tid] = v;
+    }
+    __syncthreads();
+    if (tid == 0) ctl->seq_frame += 1;
+}
+
+// ---------------------------------------------------------------------------
+// initialize (state.py:139-156)
+// ---------------------------------------------------------------------------
+__global__ void k_initialize(const cbtm_pool p, const int32_t *__restrict__ he_next,
+                             const int32_t *__restrict__ he_prev,
+                             const int32_t *__restrict__ he_twin, int n_halfedges, Control *ctl,
+                             unsigned *ticket)
+{
+    const uint64_t N = (uint64_t)1 << p.depth;
+    const uint64_t base = (uint64_t)1 << p.rank;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t gid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    for (uint64_t s = gid; s < N; s += stride) {
+        const bool root = s < (uint64_t)n_halfedges;
+        p.ids[s] = root ? base + s : 0;
+        p.nexts[s] = root ? he_next[s] : -1;
+        p.prevs[s] = root ? he_prev[s] : -1;
+        p.twins[s] = root ? he_twin[s] : -1;
+        p.commands[s] = 0;
+        reinterpret_cast<int4 *>(p.reserved)[s] = make_int4(-1, -1, -1, -1);
+        p.cache_live[s] = -1;
+        p.cache_free[s] = -1;
+    }
+    const uint64_t words = bitfield_words(p.depth);
+    for (uint64_t w = gid; w < words; w += stride) {
+        const uint64_t first = w * 64;
+        uint64_t x = 0;
+        if (first + 64 <= (uint64_t)n_halfedges) x = ~(uint64_t)0;
+        else if (first < (uint64_t)n_halfedges) x = (((uint64_t)1) << (n_halfedges - first)) - 1;
+        p.bits[w] = x;
+    }
+    if (gid == 0) {
+        p.counter[0] = 0;
+        if (p.stats)
+            for (int k = 0; k < CBTM_STATS_WORDS; ++k) p.stats[k] = 0;
+        if (ctl) {
+            ctl->n = ctl->F = ctl->T = ctl->A = 0;
+            ctl->i0 = 0;
+            ctl->tail_count = 0;
+            ctl->seq_frame = 0;
+            *ticket = 0;
+            for (int k = 0; k < CBTM_STATS_WORDS; ++k) ctl->stats[k] = 0;
+        }
+    }
+}
+
+} // namespace cbtm

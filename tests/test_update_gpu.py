@@ -1,0 +1,143 @@
+"""GPU parity: the CUDA update path (through the python drop-in, i.e. the C
+ABI) against the C oracle and the reference's golden digests, frame by frame,
+every array, bit for bit."""
+
+import numpy as np
+import pytest
+
+from paper_2407_02215_b200 import halfedge, workloads
+from paper_2407_02215_b200.pipeline import (KeepAll, MergeAll, ParallelEngine,
+                                            SplitAll, UniformSplit)
+from paper_2407_02215_b200.lod import LodDecide
+from paper_2407_02215_b200.state import initialize
+
+from tests import workloads as tw
+from tests.parity import (assert_state_equal, golden_frame_check, load_golden,
+                          stats_words)
+
+pytestmark = pytest.mark.gpu
+
+
+def run_pair(name, mesh, depth, frames, gpu_decide_of, orc_verdict_of, exact,
+             max_depth=None, golden=True, check_every=1):
+    from oracle import OraclePool
+    st = initialize(mesh, depth, exact_free_cache=exact)
+    op = OraclePool(mesh, depth)
+    if max_depth is not None:
+        st.max_depth = max_depth
+        op.max_depth = max_depth
+    rec = load_golden(name) if golden else None
+    host = assert_state_equal(st, op, f"{name}/init", exact)
+    if rec:
+        golden_frame_check(host, rec["init"], f"{name}/init", exact)
+    with ParallelEngine(threads=1) as eng:
+        for f in range(frames):
+            s = eng.update(st, gpu_decide_of(f, st), epoch=f)
+            o, _ = op.update(orc_verdict_of(f, op), threads=8)
+            assert stats_words(s) == tuple(int(x) for x in o), f"{name}/{f}: stats"
+            assert s.poison == 0
+            if f % check_every == 0 or f == frames - 1:
+                host = assert_state_equal(st, op, f"{name}/{f}", exact, s)
+                if rec:
+                    golden_frame_check(host, rec["frames"][f], f"{name}/{f}", exact)
+                    assert {k: rec["frames"][f]["stats"][k] for k in rec["frames"][f]["stats"]} == \
+                        dict(zip(("oom_splits", "oom_merges", "split_freed", "merge_freed",
+                                  "split_alloc", "merge_alloc", "live_before", "live_after"),
+                                 stats_words(s)))
+    return st, op
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_config1_quad_uniform(exact):
+    from oracle import OracleVerdict
+    st, _ = run_pair("quad_d16_uniform12", halfedge.single_quad(), 16, 18,
+                     lambda f, st: UniformSplit(12),
+                     lambda f, op: OracleVerdict.uniform(12), exact)
+    assert st.count() == 16384
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_const_sources(exact):
+    from oracle import OracleVerdict
+    run_pair("grid_d9_uniform2", halfedge.quad_grid(2, 2), 9, 3,
+             lambda f, st: UniformSplit(2), lambda f, op: OracleVerdict.uniform(2), exact)
+    run_pair("triangle_d4_splitall", halfedge.single_triangle(), 4, 6,
+             lambda f, st: SplitAll(), lambda f, op: OracleVerdict.const(1), exact)
+    consts = [SplitAll, MergeAll]
+    run_pair("grid_d12_alternate", halfedge.quad_grid(2, 2), 12, 8,
+             lambda f, st: consts[f % 2](), lambda f, op: OracleVerdict.const(1 + f % 2), exact)
+    run_pair("dodeca_d9_keep", halfedge.dodecahedron(), 9, 2,
+             lambda f, st: KeepAll(), lambda f, op: OracleVerdict.const(0), exact)
+    run_pair("triangle_d4_depthlimit1", halfedge.single_triangle(), 4, 3,
+             lambda f, st: SplitAll(), lambda f, op: OracleVerdict.const(1), exact,
+             max_depth=1)
+
+
+@pytest.mark.parametrize("case", tw.SOUP_CASES, ids=lambda c: f"{c[0]}_d{c[1]}")
+@pytest.mark.parametrize("exact", [True, False])
+def test_random_soups_under_pressure(case, exact):
+    """Explicit random verdicts, not budgeted: OOM rejections every frame, so
+    the admission tail walk and the top-of-window slot placement are pinned."""
+    from oracle import OracleVerdict
+    mesh_name, depth, seed, frames = case
+
+    def verdicts(f, n):
+        sp, mp = tw.soup_schedule(f)
+        return tw.random_verdicts(n, seed, f, sp, mp)
+
+    def gpu_decide(f, st):
+        ids = st.ids[st.live_slots()]          # ascending slot == cache_live order
+        table = {int(i): int(v) for i, v in zip(ids, verdicts(f, len(ids)))}
+        return lambda bid: table[bid]          # python-callable path of the API
+
+    run_pair(f"soup_{mesh_name}_d{depth}_s{seed}", tw.MESHES[mesh_name](), depth, frames,
+             gpu_decide, lambda f, op: OracleVerdict.explicit_array(verdicts(f, op.count())),
+             exact)
+
+
+def _lod_pair(seq):
+    from oracle import OracleVerdict
+    prms = seq.params()
+    return (lambda f, st: LodDecide(seq.config, seq.cameras[f], seq.mesh),
+            lambda f, op: OracleVerdict.lod(seq.mesh, prms[f]))
+
+
+def test_config2_cube_sphere_flyin_exact():
+    seq = workloads.cube_sphere_flyin(depth=20, frames=64)
+    g, o = _lod_pair(seq)
+    run_pair("cube_sphere_flyin_d20", seq.mesh, 20, seq.n_frames, g, o, True)
+
+
+def test_config2_cube_sphere_flyin_fast():
+    seq = workloads.cube_sphere_flyin(depth=20, frames=64)
+    g, o = _lod_pair(seq)
+    run_pair("cube_sphere_flyin_d20", seq.mesh, 20, seq.n_frames, g, o, False, check_every=4)
+
+
+def test_config3_stress_earth_sweep_d20():
+    """Config 3's camera sweep on a 2^20 pool: 727k OOM rejections."""
+    seq = workloads.earth_sweep(depth=20, frames=64)
+    g, o = _lod_pair(seq)
+    run_pair("earth_sweep_d20", seq.mesh, 20, seq.n_frames, g, o, True, check_every=4)
+
+
+def test_config3_short_d22():
+    seq = workloads.earth_sweep(depth=22, frames=16)
+    g, o = _lod_pair(seq)
+    run_pair("earth_sweep_d22_short", seq.mesh, 22, seq.n_frames, g, o, False, check_every=8)
+
+
+def test_sequence_runner_matches_per_frame_updates():
+    """cbtm_run_lod_sequence (no host sync between frames) == frame-by-frame."""
+    seq = workloads.cube_sphere_flyin(depth=18, frames=24)
+    a = initialize(seq.mesh, 18)
+    b = initialize(seq.mesh, 18)
+    with ParallelEngine() as eng:
+        per_frame = [eng.update(a, LodDecide(seq.config, c, seq.mesh), epoch=i)
+                     for i, c in enumerate(seq.cameras)]
+        batched = eng.run_lod_sequence(b, seq.params())
+    assert [stats_words(s) for s in per_frame] == [stats_words(s) for s in batched]
+    ha, hb = a.to_host(), b.to_host()
+    for k in ha:
+        if k != "cache_free":
+            assert np.array_equal(ha[k], hb[k]), k
