@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""bench.py -- per-frame bisector update on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+A *step* is one full nine-stage update (index + classify + admit + split/merge +
+bitfield + sum reduction) of one planet for one camera frame.  The workload at
+N = 1 is BASELINE config 3: the Earth-scale icosphere planet on a 2^26-slot pool,
+LOD camera sweeping between the ground (10 m) and space (3 R).  Untimed setup
+flies the camera down to the ground (64 frames); the warm-up and timed steps then
+ride the ground<->space sweep (period 128 frames), so the pool keeps splitting
+and merging for any K.  With N > 1 every rank owns one such planet (camera path
+rotated by rank * 45 degrees, as BASELINE config 5 rotates its planets): weak
+scaling, no data-path collective, one final gather of the per-rank stats.
+
+Reported on ONE JSON line (rank 0):
+  value / ms_per_step  device-timed (CUDA events on the launch stream) K-step run
+                       through cbtm_run_lod_sequence, camera parameters already
+                       resident in HBM, no host synchronisation between frames
+  e2e                  the same K frames through the public python API
+                       (ParallelEngine.update + LodDecide per frame): per-frame
+                       host->device camera parameters and device->host stats read
+  roofline             the sum-reduction kernel (dominant full-pool pass) timed
+                       alone with CUDA events, L2 flushed between launches
+  cpu_baseline         the oracle port of the reference CPU path on this box's
+                       host cores, on a bounded sample of the same frames, started
+                       from the same pool state (also a parity check of the run)
+
+--impl reference runs the reference's CPU algorithm (oracle port, all host
+threads) on the same workload: CPU only, none of the CUDA code.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "update ms/frame & bisectors/s (classify+split/merge+CBT reduce+index)"
+UNIT = "bisectors/s"
+SETUP_FRAMES = 64
+
+
+def sweep_params(depth: int, rotate_deg: float):
+    """(mesh, config, descent prm[64,23], cyclic sweep prm[128,23])."""
+    from paper_2407_02215_b200 import workloads
+    seq = workloads.earth_sweep(depth=depth, frames=SETUP_FRAMES, rotate_deg=rotate_deg)
+    prm = seq.params()
+    down = prm[:SETUP_FRAMES]
+    cycle = np.concatenate([down[::-1], down])  # ascent, then descent again
+    return seq, down, cycle
+
+
+def step_params(cycle: np.ndarray, first: int, count: int) -> np.ndarray:
+    idx = (first + np.arange(count)) % cycle.shape[0]
+    return np.ascontiguousarray(cycle[idx])
+
+
+def load_peaks() -> tuple[float, str]:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.rows = []
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._pump, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for name, cell in zip(names, r[5:9]):
+                if cell.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# CPU arms (oracle port of the reference path)
+# ---------------------------------------------------------------------------
+
+def oracle_pool_from_host(mesh, depth, host_arrays):
+    from oracle import OraclePool
+    op = OraclePool(mesh, depth)
+    for k, v in host_arrays.items():
+        getattr(op, k)[...] = v
+    return op
+
+
+def cpu_sample(op, mesh, prms, threads):
+    """Time len(prms) genuine oracle frames; returns (seconds, stats rows)."""
+    from oracle import OracleVerdict
+    rows, total = [], 0.0
+    for prm in prms:
+        t0 = time.perf_counter()
+        s, _ = op.update(OracleVerdict.lod(mesh, prm), threads=threads)
+        total += time.perf_counter() - t0
+        rows.append([int(x) for x in s])
+    return total, rows
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU algorithm (oracle port), CPU only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    from oracle import OraclePool, OracleVerdict
+    threads = oracle.max_threads()
+    seq, down, cycle = sweep_params(args.depth, 0.0)
+    op = OraclePool(seq.mesh, args.depth)
+    for prm in down:  # untimed setup: fast-forward with the linear-scan stage 2
+        op.update(OracleVerdict.lod(seq.mesh, prm), threads=threads, fast_setup=True)
+    for prm in step_params(cycle, 0, args.warmup):
+        op.update(OracleVerdict.lod(seq.mesh, prm), threads=threads)
+    seconds, rows = cpu_sample(op, seq.mesh, step_params(cycle, args.warmup, args.steps), threads)
+    units = sum(r[6] for r in rows)
+    value = units / seconds
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * seconds / max(1, args.steps), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32/u64 + f64 classifier",
+        "data": "synthetic", "config": workload_config(args, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} full frames of the workload (oracle port of the "
+                                   "reference path, OpenMP over stage 2 / classifier / stage 9)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def workload_config(args, n_gpus):
+    return {"workload": f"earth_sweep icosphere H=240, pool 2^{args.depth} slots, LOD camera "
+                        f"ground(10 m)<->space(3R) sweep 1920x1080, 49 px target; "
+                        f"{SETUP_FRAMES} untimed descent frames then steps ride the 128-frame cycle",
+            "pool_depth": args.depth, "planets": n_gpus,
+            "parallelism": "1 planet per GPU, no collective on the data path",
+            "l2": "pool state (3.3 GB) exceeds L2; roofline kernel timed with L2 flushed"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_02215_b200 import _lib
+    from paper_2407_02215_b200.lod import LodDecide
+    from paper_2407_02215_b200.pipeline import ParallelEngine
+    from paper_2407_02215_b200.state import initialize
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (there is no CPU fallback for the product path)")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    seq, down, cycle = sweep_params(args.depth, 45.0 * rank)
+    K, W = args.steps, args.warmup
+    eng = ParallelEngine()
+    state = initialize(seq.mesh, args.depth, device=device)
+    eng.run_lod_sequence(state, down)                       # setup: fly to the ground
+    eng.run_lod_sequence(state, step_params(cycle, 0, W))   # warm-up steps
+    timed_prm = step_params(cycle, W, K)
+
+    start_host = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        start_host = state.to_host()
+    e2e_state = state.clone()
+
+    # ---- device-timed run: K frames, parameters resident, no host sync ----
+    L = _lib.load()
+    import ctypes as C
+    d_stats = torch.zeros((K, _lib.STATS_WORDS), dtype=torch.int64, device=device)
+    pinned = torch.from_numpy(timed_prm).pin_memory()
+    pool = state.c_pool()
+    sampler = ClockSampler(local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if rank == 0:
+        sampler.start()
+    barrier()
+    ev0.record()
+    rc = L.cbtm_run_lod_sequence(C.byref(pool), _lib.ptr(state.d_root_tris), pinned.data_ptr(), K,
+                                 _lib.ptr(d_stats), state.stream())
+    ev1.record()
+    barrier()
+    _lib.check(rc, "cbtm_run_lod_sequence")
+    state._touched()
+    gpu_ms = ev0.elapsed_time(ev1)
+    clocks = sampler.stop() if rank == 0 else None
+    rows = d_stats.cpu().numpy()
+    units = int(rows[:, 6].sum())
+
+    # ---- e2e: same frames through the public API, per-frame host<->device ----
+    cams = seq.cameras
+    cam_cycle = cams[SETUP_FRAMES - 1::-1] + cams[:SETUP_FRAMES]
+    barrier()
+    t0 = time.perf_counter()
+    e2e_rows = []
+    for j in range(K):
+        cam = cam_cycle[(W + j) % len(cam_cycle)]
+        s = eng.update(e2e_state, LodDecide(seq.config, cam, seq.mesh), epoch=j)
+        e2e_rows.append(s)
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    same = all(torch.equal(getattr(state, "d_" + k), getattr(e2e_state, "d_" + k))
+               for k in ("ids", "nexts", "prevs", "twins", "commands", "reserved", "bits", "counters"))
+    if not same:
+        raise SystemExit("bench.py: e2e run and device-timed run diverged (parity failure)")
+
+    # ---- max over ranks ----
+    t = torch.tensor([gpu_ms, e2e_s * 1e3, float(units)], dtype=torch.float64, device=device)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        gpu_ms, e2e_ms, units_all = float(tmax[0]), float(tmax[1]), float(tsum[2])
+        gathered = [torch.zeros_like(d_stats) for _ in range(world)]
+        dist.all_gather(gathered, d_stats)  # the only collective: final stats gather
+    else:
+        e2e_ms, units_all = e2e_s * 1e3, float(units)
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline: the sum-reduction kernel alone, L2 flushed between launches ----
+    peak, peak_src = load_peaks()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    reps = 20
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in evs:
+        flush.fill_(1)
+        a.record()
+        L.cbtm_sum_reduce(_lib.ptr(state.d_bits), _lib.ptr(state.d_counters), args.depth,
+                          _lib.ptr(state.d_workspace), state.d_workspace.numel(), state.stream())
+        b.record()
+    torch.cuda.synchronize(device)
+    red_ms = float(np.median([a.elapsed_time(b) for a, b in evs]))
+    N = 1 << args.depth
+    red_bytes = N // 8 + 4 * L.cbtm_counter_words(args.depth)
+    achieved = red_bytes / (red_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "k_sum_reduce", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "algorithmic_bytes": red_bytes, "kernel_ms": red_ms, "peak_source": peak_src,
+                "note": "N/8 bitfield bytes read + 4*(2<<Lc) counter bytes written per launch"}
+
+    # ---- CPU baseline on a bounded sample, from the same start state ----
+    cpu = None
+    if start_host is not None:
+        import oracle
+        threads = oracle.max_threads()
+        n_cpu = min(K, args.cpu_frames)
+        op = oracle_pool_from_host(seq.mesh, args.depth, start_host)
+        sec, cpu_rows = cpu_sample(op, seq.mesh, timed_prm[:n_cpu], threads)
+        for j in range(n_cpu):
+            if cpu_rows[j] != [int(x) for x in rows[j, :8]]:
+                raise SystemExit(f"bench.py: GPU and CPU-oracle stats differ at timed frame {j}: "
+                                 f"{rows[j, :8].tolist()} vs {cpu_rows[j]}")
+        cpu_units = sum(r[6] for r in cpu_rows)
+        cpu = {"value": cpu_units / sec, "unit": UNIT, "cores": threads, "kind": "port",
+               "ms_per_frame": 1e3 * sec / n_cpu,
+               "sample": f"first {n_cpu} timed frames from the same pool state (stats verified "
+                         "equal to the GPU's), oracle port with OpenMP stage 2/classify/stage 9"}
+
+    launches_per_frame = 10  # index, classify, admit, scatter, agree, alloc_scan, reserve, apply, reduce, publish
+    line = {
+        "metric": METRIC, "value": units_all / (gpu_ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": gpu_ms / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32/u64 + f64 classifier",
+        "data": "synthetic", "config": workload_config(args, world),
+        "live_bisectors_per_frame": {"mean": float(rows[:, 6].mean()), "max": int(rows[:, 6].max())},
+        "ops_in_run": {"splits": int(rows[:, 2].sum()), "merges": int(rows[:, 3].sum()),
+                       "oom": int(rows[:, 0].sum() + rows[:, 1].sum())},
+        "e2e": {"value": units_all / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms / K,
+                "h2d_bytes_per_step": 8 * _lib.PRM_WORDS, "d2h_bytes_per_step": 8 * _lib.STATS_WORDS,
+                "note": "pool state is device-resident by design; per-frame host input is the camera"},
+        "gpu_launches": launches_per_frame * K,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", default="graft", choices=["graft", "reference"])
+    ap.add_argument("--depth", type=int, default=26)
+    ap.add_argument("--cpu-frames", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -535,6 +535,22 @@ void orc_cache_pointers(orc_pool *p, int64_t count, int64_t free_ct,
     (void)threads;
 }
 
+/* Same output as orc_cache_pointers (ascending positions of set / unset bits,
+ * kernels.py:244-252) by one linear pass over the leaves.  NOT the reference's
+ * algorithm: used only to fast-forward untimed setup frames of the CPU
+ * baseline; every timed or parity-checked frame uses the descents above. */
+void orc_cache_pointers_scan(orc_pool *p)
+{
+    const uint32_t *leaves = p->nodes + p->capacity;
+    int64_t n1 = 0, n0 = 0;
+    for (int64_t s = 0; s < p->capacity; ++s) {
+        if (leaves[s])
+            p->cache_live[n1++] = (int32_t)s;
+        else
+            p->cache_free[n0++] = (int32_t)s;
+    }
+}
+
 /* stage 3, kernels.py:255-259 */
 void orc_reset_commands(orc_pool *p, int64_t start, int64_t end)
 {
@@ -856,6 +872,9 @@ static int64_t now_ns(void)
 int orc_update(orc_pool *p, const orc_verdict *v, int8_t *verdict_scratch,
                int64_t *stats8, int64_t *stage_ns, int threads)
 {
+    const int fast_setup = threads < 0; /* untimed setup frames, see orc_cache_pointers_scan */
+    if (fast_setup)
+        threads = -threads;
     const int64_t count = p->nodes[1];
     const int64_t free_ct = p->capacity - count;
     int64_t stats6[6] = {0, 0, 0, 0, 0, 0};
@@ -866,7 +885,10 @@ int orc_update(orc_pool *p, const orc_verdict *v, int8_t *verdict_scratch,
     t[0] = now_ns();
     p->counter[0] = 0; /* (1) */
     t[1] = now_ns();
-    orc_cache_pointers(p, count, free_ct, 0, count > free_ct ? count : free_ct, threads); /* (2) */
+    if (fast_setup)
+        orc_cache_pointers_scan(p);
+    else
+        orc_cache_pointers(p, count, free_ct, 0, count > free_ct ? count : free_ct, threads); /* (2) */
     t[2] = now_ns();
     orc_reset_commands(p, 0, count); /* (3) */
     t[3] = now_ns();

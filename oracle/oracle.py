@@ -204,8 +204,13 @@ class OraclePool:
     def live_slots(self) -> np.ndarray:
         return np.flatnonzero(self.leaves).astype(np.int32)
 
-    def update(self, verdict: OracleVerdict, threads: int = 1):
-        """One frame.  Returns (stats8, stage_ns9) as int64 arrays."""
+    def update(self, verdict: OracleVerdict, threads: int = 1,
+               fast_setup: bool = False):
+        """One frame.  Returns (stats8, stage_ns9) as int64 arrays.
+        fast_setup=True replaces the stage-2 descents by a linear scan with the
+        same output (untimed fast-forwarding only, never for parity/timing)."""
+        if fast_setup:
+            threads = -max(1, threads)
         cv = _CVerdict()
         cv.mode, cv.value = verdict.mode, verdict.value
         keep = []
