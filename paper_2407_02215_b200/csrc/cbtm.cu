@@ -39,15 +39,36 @@ inline unsigned strided_grid(uint64_t units, uint64_t per_cta, int ctas_per_sm)
 }
 
 int reduce_launch(const uint64_t *bits, uint32_t *counters, int depth, unsigned *ticket,
-                  int64_t *live_after, cudaStream_t st)
+                  const ReducePublish &pub, cudaStream_t st)
 {
+    static bool smem_opt_in = false;
+    if (!smem_opt_in) {
+        const cudaError_t e = cudaFuncSetAttribute(k_sum_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   RED_MAX_STAGES * RED_TILE_BYTES);
+        if (e != cudaSuccess) return status(e);
+        smem_opt_in = true;
+    }
     const Geo g = make_geo(depth);
     const unsigned tiles = g.nblocks > (unsigned)RED_TILE_BLOCKS ? g.nblocks / RED_TILE_BLOCKS : 1u;
-    const uint32_t n_vec = (uint32_t)(bitfield_words(depth) / 2);
-    k_sum_reduce<<<tiles, RED_THREADS, 0, st>>>(reinterpret_cast<const uint4 *>(bits), counters, g.lc,
-                                                n_vec, ticket, live_after);
+    const uint64_t total_bytes = (uint64_t)bitfield_words(depth) * 8;
+    // few tiles: one CTA per tile, all resident; many: 3 CTAs per SM, each streaming
+    // its range through a 4-stage (64 KB) ring
+    unsigned grid = tiles;
+    int stages = 1;
+    const unsigned resident = (unsigned)sm_count() * 4;
+    if (tiles > resident) {
+        grid = (unsigned)sm_count() * 3;
+        const unsigned per_cta = (tiles + grid - 1) / grid;
+        stages = per_cta < (unsigned)RED_MAX_STAGES ? (int)per_cta : RED_MAX_STAGES;
+    }
+    // the last CTA reuses the ring as a heap of 2 * tiles words
+    while ((size_t)stages * RED_TILE_BYTES < (size_t)tiles * 8) ++stages;
+    k_sum_reduce<<<grid, RED_THREADS, (size_t)stages * RED_TILE_BYTES, st>>>(
+        reinterpret_cast<const uint8_t *>(bits), counters, g.lc, total_bytes, tiles, stages, ticket, pub);
     return launch_status();
 }
+
+const ReducePublish kNoPublish = {nullptr, nullptr, nullptr, nullptr};
 
 int check_pool(const cbtm_pool *p, bool need_ws)
 {
@@ -121,10 +142,8 @@ int finish_launch(const FrameArgs &a, int64_t *stats_seq, cudaStream_t st)
     k_apply<<<grid, CHUNK, 0, st>>>(a);
     int rc = launch_status();
     if (rc) return rc;
-    rc = reduce_launch(a.pool.bits, a.pool.counters, a.pool.depth, a.ws.ticket, nullptr, st);
-    if (rc) return rc;
-    k_publish<<<1, 32, 0, st>>>(a, stats_seq);
-    return launch_status();
+    const ReducePublish pub = {a.ws.ctl->stats, a.pool.stats, stats_seq, &a.ws.ctl->seq_frame};
+    return reduce_launch(a.pool.bits, a.pool.counters, a.pool.depth, a.ws.ticket, pub, st);
 }
 
 } // namespace
@@ -152,7 +171,7 @@ int cbtm_sum_reduce(const uint64_t *bits, uint32_t *counters, int depth, void *w
     if (workspace_bytes < 256) return CBTM_E_WORKSPACE;
     // the ticket is word 0 of the workspace (also of a pool's frame workspace); it
     // must be zero on entry and the last CTA leaves it zero again
-    return reduce_launch(bits, counters, depth, reinterpret_cast<unsigned *>(workspace), nullptr,
+    return reduce_launch(bits, counters, depth, reinterpret_cast<unsigned *>(workspace), kNoPublish,
                          as_stream(stream));
 }
 
@@ -224,7 +243,7 @@ int cbtm_initialize(const cbtm_pool *pool, const int32_t *he_next, const int32_t
         *pool, he_next, he_prev, he_twin, n_halfedges, ws.ctl, ws.ticket);
     rc = launch_status();
     if (rc) return rc;
-    return reduce_launch(pool->bits, pool->counters, pool->depth, ws.ticket, nullptr, st);
+    return reduce_launch(pool->bits, pool->counters, pool->depth, ws.ticket, kNoPublish, st);
 }
 
 int cbtm_root_triangles(const int32_t *he_next, const int32_t *he_vert, const double *positions,

@@ -10,91 +10,221 @@ namespace cbtm {
 // ---------------------------------------------------------------------------
 // Sum reduction (Cbt.sum_reduce, cbt.py:61-68; pipeline stage 9).
 //
-// One CTA reduces a tile of 2^17 slots (16 KB of bitfield = 128 leaf blocks):
-// four independent 128-bit loads per thread, popcount, 8-lane shuffle to a
-// leaf-block count, then seven tree levels in shared memory.  The 255 tile
-// nodes are written level by level (coalesced).  The last CTA to finish
-// (ticket) builds the levels above the tile roots in shared memory.
+// A tile is 2^17 slots = 16 KB of bitfield = 128 leaf blocks.  Tiles are dealt
+// round-robin to the CTAs, which stream them through a ring of 16 KB shared
+// memory stages filled by TMA bulk copies (cp.async.bulk + mbarrier
+// complete_tx): one elected thread keeps up to `stages` tiles in flight, so the
+// HBM pipe stays full without spending registers or LSU issue slots on it.
+// Every thread then owns 64 contiguous bytes of the tile (four conflict-free
+// 128-bit shared loads in a lane-rotated order), so a leaf block is a lane
+// pair and the warp's five tree levels (16+8+4+2+1 nodes) fall out of five
+// shuffle butterflies; disjoint lanes hold one node each and write all 31 with
+// a single store instruction.  The three levels that join the eight warps cost
+// the one CTA barrier per tile that also recycles the stage.  Levels above the
+// tile roots are built by the last CTA to finish (ticket; only thread 0
+// fences -- the fence is cumulative over the preceding barrier).
 // HBM traffic: N/8 bytes read + 4 * (2 << Lc) = N/128 bytes written.
 // ---------------------------------------------------------------------------
 constexpr int RED_THREADS = 256;
-constexpr int RED_LOADS = 4;
-constexpr int RED_TILE_VEC = RED_THREADS * RED_LOADS; // uint4 per tile
-constexpr int RED_TILE_BLOCKS = RED_TILE_VEC / 8;     // leaf blocks per tile = 128
-constexpr int RED_TILE_LOG2 = 7;
-constexpr int RED_UPPER_MAX = 4096; // tile roots handled in shared memory
+constexpr int RED_TILE_BYTES = 16384;
+constexpr int RED_TILE_BLOCKS = 128; // leaf blocks per tile
+constexpr int RED_MAX_STAGES = 4;
+
+// end-of-frame bookkeeping folded into the last CTA (all NULL when standalone)
+struct ReducePublish {
+    int64_t *ctl_stats;  // Control::stats
+    int64_t *pool_stats; // cbtm_pool::stats
+    int64_t *stats_seq;  // per-frame rows of a sequence run
+    uint32_t *seq_frame; // Control::seq_frame
+};
+
+__device__ __forceinline__ void publish_frame(const ReducePublish &pub, uint32_t live_after, int tid)
+{
+    if (!pub.ctl_stats) return;
+    if (tid < CBTM_STATS_WORDS) {
+        int64_t v = pub.ctl_stats[tid];
+        if (tid == CBTM_STAT_LIVE_AFTER) v = live_after;
+        if (tid == CBTM_STAT_FRAME) {
+            v += 1;
+            pub.ctl_stats[tid] = v;
+        }
+        if (pub.pool_stats) pub.pool_stats[tid] = v;
+        if (pub.stats_seq) pub.stats_seq[(size_t)CBTM_STATS_WORDS * (*pub.seq_frame) + tid] = v;
+    }
+    __syncwarp();
+    if (tid == 0) *pub.seq_frame += 1;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra DONE_%=;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// TMA 1-D bulk copy global -> shared, completion signalled on an mbarrier
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 
 __global__ void __launch_bounds__(RED_THREADS)
-k_sum_reduce(const uint4 *__restrict__ bits, uint32_t *__restrict__ counters, int lc,
-             uint32_t n_vec, unsigned *ticket, int64_t *live_after)
+k_sum_reduce(const uint8_t *__restrict__ bits, uint32_t *__restrict__ counters, int lc,
+             uint64_t total_bytes, uint32_t n_tiles, int stages, unsigned *ticket,
+             const ReducePublish pub)
 {
-    __shared__ uint32_t tree[2 * RED_TILE_BLOCKS];
-    __shared__ uint32_t upper[2 * RED_UPPER_MAX];
+    extern __shared__ __align__(128) uint8_t ring[]; // stages x 16 KB
+    __shared__ __align__(8) uint64_t full[RED_MAX_STAGES];
+    __shared__ uint32_t wroot[2][RED_THREADS / 32];
     __shared__ bool is_last;
 
-    const int t = threadIdx.x;
-    const uint32_t tile = blockIdx.x;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    // tiles are dealt round-robin (tile = blockIdx.x + k * gridDim.x): at any moment the
+    // CTAs read one contiguous window of the bitfield, which keeps DRAM rows open
+    const uint32_t tile0 = blockIdx.x, tile_step = gridDim.x;
+    const uint32_t my_tiles = tile0 < n_tiles ? (n_tiles - tile0 + tile_step - 1) / tile_step : 0u;
 
-    uint4 v[RED_LOADS];
-#pragma unroll
-    for (int j = 0; j < RED_LOADS; ++j) {
-        const uint32_t idx = tile * RED_TILE_VEC + j * RED_THREADS + t;
-        v[j] = idx < n_vec ? ld_stream(bits + idx) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int j = 0; j < RED_LOADS; ++j) {
-        uint32_t c = popc128(v[j]);
-        c += __shfl_xor_sync(FULL_MASK, c, 1);
-        c += __shfl_xor_sync(FULL_MASK, c, 2);
-        c += __shfl_xor_sync(FULL_MASK, c, 4);
-        if ((t & 7) == 0) tree[RED_TILE_BLOCKS + j * (RED_THREADS / 8) + (t >> 3)] = c;
+    auto tile_bytes = [&](uint32_t tile) -> uint32_t {
+        const uint64_t left = total_bytes - (uint64_t)tile * RED_TILE_BYTES;
+        return left < RED_TILE_BYTES ? (uint32_t)left : (uint32_t)RED_TILE_BYTES;
+    };
+    auto issue = [&](uint32_t tile, int stage) {
+        const uint32_t bytes = tile_bytes(tile);
+        mbar_expect_tx(&full[stage], bytes);
+        bulk_load(ring + (size_t)stage * RED_TILE_BYTES, bits + (size_t)tile * RED_TILE_BYTES, bytes,
+                  &full[stage]);
+    };
+
+    if (t == 0) {
+        for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    if (t == 0)
+        for (uint32_t k = 0; k < (uint32_t)stages && k < my_tiles; ++k) issue(tile0 + k * tile_step, (int)k);
+
+    for (uint32_t k = 0; k < my_tiles; ++k) {
+        const uint32_t tile = tile0 + k * tile_step;
+        const int stage = (int)(k % (uint32_t)stages);
+        mbar_wait(&full[stage], (k / (uint32_t)stages) & 1u);
+
+        // my 64 bytes of the tile; the rotation keeps the four LDS.128 conflict free
+        const uint4 *mine = reinterpret_cast<const uint4 *>(ring + (size_t)stage * RED_TILE_BYTES) + t * 4;
+        uint32_t c = 0;
 #pragma unroll
-    for (int w = RED_TILE_BLOCKS / 2; w >= 1; w >>= 1) {
-        if (t < w) tree[w + t] = tree[2 * (w + t)] + tree[2 * (w + t) + 1];
-        __syncthreads();
-    }
-    // local heap node t (level ll, position pos) is global level lc - 7 + ll
-    if (t >= 1) {
-        const int ll = 31 - __clz(t);
-        const uint32_t pos = t - (1u << ll);
-        const int gl = lc - RED_TILE_LOG2 + ll;
-        if (gl >= 0 && (gridDim.x > 1 || pos < (1u << gl))) {
-            counters[(1u << gl) + tile * (1u << ll) + pos] = tree[t];
-            if (gl == 0 && live_after) *live_after = tree[t];
+        for (int j = 0; j < 4; ++j) c += popc128(mine[(j + (lane >> 1)) & 3]);
+        if ((uint32_t)t * 64u >= tile_bytes(tile)) c = 0; // partial tile of a tiny pool
+
+        // butterflies: l0 leaf block (lane pair) ... l4 all 16 leaf blocks of the warp
+        const uint32_t l0 = c + __shfl_xor_sync(FULL_MASK, c, 1);
+        const uint32_t l1 = l0 + __shfl_xor_sync(FULL_MASK, l0, 2);
+        const uint32_t l2 = l1 + __shfl_xor_sync(FULL_MASK, l1, 4);
+        const uint32_t l3 = l2 + __shfl_xor_sync(FULL_MASK, l2, 8);
+        const uint32_t l4 = l3 + __shfl_xor_sync(FULL_MASK, l3, 16);
+
+        uint32_t val = 0, pos = 0;
+        int lvl = -1;
+        if ((lane & 1) == 0) {
+            val = l0, lvl = lc, pos = tile * 128 + warp * 16 + (lane >> 1);
+        } else if ((lane & 3) == 1) {
+            val = l1, lvl = lc - 1, pos = tile * 64 + warp * 8 + (lane >> 2);
+        } else if ((lane & 7) == 3) {
+            val = l2, lvl = lc - 2, pos = tile * 32 + warp * 4 + (lane >> 3);
+        } else if ((lane & 15) == 7) {
+            val = l3, lvl = lc - 3, pos = tile * 16 + warp * 2 + (lane >> 4);
+        } else if (lane == 15) {
+            val = l4, lvl = lc - 4, pos = tile * 8 + warp;
+        }
+        if (lvl >= 0 && pos < (1u << lvl)) counters[(1u << lvl) + pos] = val;
+        if (lane == 0) wroot[k & 1][warp] = l4;
+        __syncthreads(); // stage consumed by everyone; warp roots visible
+        if (t == 0 && k + (uint32_t)stages < my_tiles) issue(tile + (uint32_t)stages * tile_step, stage);
+        if (warp == 0 && lane < 7) { // levels lc-5 (4 nodes), lc-6 (2), lc-7 (tile root)
+            const uint32_t *w = wroot[k & 1];
+            uint32_t v2, p2;
+            int l5;
+            if (lane < 4) {
+                v2 = w[2 * lane] + w[2 * lane + 1], l5 = lc - 5, p2 = tile * 4 + lane;
+            } else if (lane < 6) {
+                const int q = (lane - 4) * 4;
+                v2 = w[q] + w[q + 1] + w[q + 2] + w[q + 3], l5 = lc - 6, p2 = tile * 2 + (lane - 4);
+            } else {
+                v2 = w[0] + w[1] + w[2] + w[3] + w[4] + w[5] + w[6] + w[7], l5 = lc - 7, p2 = tile;
+            }
+            if (l5 >= 0 && p2 < (1u << l5)) counters[(1u << l5) + p2] = v2;
         }
     }
-    if (gridDim.x == 1) return;
+
+    if (n_tiles == 1) { // the single tile's subtree is the whole tree
+        const uint32_t *w = wroot[0];
+        publish_frame(pub, w[0] + w[1] + w[2] + w[3] + w[4] + w[5] + w[6] + w[7], t);
+        return;
+    }
 
     // ---- levels above the tile roots: last CTA standing ----
-    __threadfence();
     __syncthreads();
-    if (t == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    if (t == 0) {
+        __threadfence();
+        is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
     __syncthreads();
     if (!is_last) return;
     __threadfence();
 
-    uint32_t cnt = gridDim.x; // nodes on the tile-root level, a power of two
-    while (cnt > RED_UPPER_MAX) {
-        const uint32_t half = cnt >> 1;
-        for (uint32_t i = t; i < half; i += RED_THREADS)
-            counters[half + i] = __ldcg(&counters[cnt + 2 * i]) + __ldcg(&counters[cnt + 2 * i + 1]);
-        __syncthreads();
-        cnt = half;
+    // Upper tree as a binary heap in the (now idle) ring: coalesced L2 loads of the
+    // tile roots, issued eight at a time per thread so they overlap; log2(cnt)
+    // levels in shared memory; one coalesced copy-out of all internal nodes.
+    // (Walking the levels through L2 instead costs a round trip per level.)
+    uint32_t *heap = reinterpret_cast<uint32_t *>(ring); // 2 * cnt words <= stages * 16 KB
+    const uint32_t cnt = n_tiles;                        // power of two, 2 .. 8192
+    for (uint32_t base = 0; base < cnt; base += 8 * RED_THREADS) {
+        uint32_t r[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t i = base + u * RED_THREADS + t;
+            r[u] = i < cnt ? __ldcg(&counters[cnt + i]) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t i = base + u * RED_THREADS + t;
+            if (i < cnt) heap[cnt + i] = r[u];
+        }
     }
-    for (uint32_t i = t; i < cnt; i += RED_THREADS) upper[cnt + i] = __ldcg(&counters[cnt + i]);
     __syncthreads();
     for (uint32_t w = cnt >> 1; w >= 1; w >>= 1) {
-        for (uint32_t i = t; i < w; i += RED_THREADS)
-            upper[w + i] = upper[2 * (w + i)] + upper[2 * (w + i) + 1];
+        for (uint32_t i = t; i < w; i += RED_THREADS) heap[w + i] = heap[2 * (w + i)] + heap[2 * (w + i) + 1];
         __syncthreads();
     }
-    for (uint32_t i = 1 + t; i < cnt; i += RED_THREADS) counters[i] = upper[i];
-    if (t == 0) {
-        *ticket = 0;
-        if (live_after) *live_after = upper[1];
-    }
+    for (uint32_t i = 1 + t; i < cnt; i += RED_THREADS) counters[i] = heap[i];
+    if (t == 0) *ticket = 0;
+    publish_frame(pub, heap[1], t);
 }
 
 // ---------------------------------------------------------------------------
@@ -162,6 +292,11 @@ k_decode(const uint64_t *__restrict__ bits, const uint32_t *__restrict__ counter
 // ---------------------------------------------------------------------------
 constexpr int IDX_WARPS = 8;
 
+// staging index swizzle: element i lives at i ^ ((i >> 5) & 31).  Expansion
+// writes from different lanes are typically ~32 apart (same bank unswizzled);
+// the copy-out reads 32 consecutive elements, which stay conflict free.
+__device__ __forceinline__ uint32_t stage_at(uint32_t i) { return i ^ ((i >> 5) & 31u); }
+
 __global__ void __launch_bounds__(IDX_WARPS * 32)
 k_index(const uint32_t *__restrict__ bits32, const uint32_t *__restrict__ counters, int depth,
         int32_t *__restrict__ cache_live, int32_t *__restrict__ cache_free,
@@ -220,20 +355,20 @@ k_index(const uint32_t *__restrict__ bits32, const uint32_t *__restrict__ counte
         while (ones) {
             const int k = __ffs(ones) - 1;
             ones &= ones - 1;
-            st[o1++] = lane_base + k;
+            st[stage_at(o1++)] = lane_base + k;
         }
         if (cache_free) {
             uint32_t zeros = ~w & vmask;
             while (zeros) {
                 const int k = __ffs(zeros) - 1;
                 zeros &= zeros - 1;
-                st[o0++] = lane_base + k;
+                st[stage_at(o0++)] = lane_base + k;
             }
         }
         __syncwarp();
-        for (uint32_t i = lane; i < cnt; i += 32) cache_live[ones_before + i] = st[i];
+        for (uint32_t i = lane; i < cnt; i += 32) cache_live[ones_before + i] = st[stage_at(i)];
         if (cache_free)
-            for (uint32_t i = lane; i < zcnt; i += 32) cache_free[zeros_before + i] = st[cnt + i];
+            for (uint32_t i = lane; i < zcnt; i += 32) cache_free[zeros_before + i] = st[stage_at(cnt + i)];
         __syncwarp();
     }
 }

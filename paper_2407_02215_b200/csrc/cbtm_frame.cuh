@@ -18,7 +18,7 @@
 //
 // Launch order per frame (all on one stream, no host synchronisation):
 //   k_classify -> k_admit -> k_scatter -> k_agree -> k_alloc_scan -> k_reserve
-//   -> k_apply -> k_sum_reduce
+//   -> k_apply -> k_sum_reduce (its last CTA also publishes the frame's stats)
 #pragma once
 
 #include "cbtm_cbt.cuh"
@@ -848,23 +848,6 @@ k_apply(const __grid_constant__ FrameArgs a)
         const int slot = tid < 4 ? CBTM_STAT_SPLIT_FREED + tid : CBTM_STAT_POISON;
         atomicAdd((unsigned long long *)&a.ws.ctl->stats[slot], (unsigned long long)acc[tid]);
     }
-}
-
-// end of frame: publish the stats block, advance the sequence frame counter
-__global__ void k_publish(const __grid_constant__ FrameArgs a, int64_t *__restrict__ stats_seq)
-{
-    Control *ctl = a.ws.ctl;
-    const int tid = threadIdx.x;
-    if (tid < CBTM_STATS_WORDS) {
-        int64_t v = ctl->stats[tid];
-        if (tid == CBTM_STAT_LIVE_AFTER) v = a.pool.counters[1];
-        if (tid == CBTM_STAT_FRAME) v += 1;
-        if (a.pool.stats) a.pool.stats[tid] = v;
-        if (stats_seq) stats_seq[(size_t)CBTM_STATS_WORDS * ctl->seq_frame + tid] = v;
-        if (tid == CBTM_STAT_FRAME) ctl->stats[tid] = v;
-    }
-    __syncthreads();
-    if (tid == 0) ctl->seq_frame += 1;
 }
 
 // ---------------------------------------------------------------------------
