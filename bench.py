@@ -429,6 +429,8 @@ def run_gpu(args):
         "live_bisectors_per_frame": {"mean": float(rows[:, 6].mean()), "max": int(rows[:, 6].max())},
         "ops_in_run": {"splits": int(rows[:, 2].sum()), "merges": int(rows[:, 3].sum()),
                        "oom": int(rows[:, 0].sum() + rows[:, 1].sum())},
+        "phase_us": {name: float(rows[:, _lib.STAT_PHASE_NS + k].mean()) / 1e3
+                     for k, name in enumerate(_lib.PHASE_NAMES)},
         "e2e": {"value": units_all / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms / K,
                 "h2d_bytes_per_step": 8 * _lib.PRM_WORDS, "d2h_bytes_per_step": 8 * _lib.STATS_WORDS,
                 "note": "pool state is device-resident by design; per-frame host input is the camera"},

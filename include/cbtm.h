@@ -40,7 +40,7 @@ extern "C" {
 #define CBTM_MIN_DEPTH 1
 #define CBTM_MAX_DEPTH 30 /* slot indices are int32; counters are uint32 */
 #define CBTM_LEAF_BLOCK_LOG2 10
-#define CBTM_STATS_WORDS 16
+#define CBTM_STATS_WORDS 32
 #define CBTM_PRM_WORDS 23
 
 /* contract violations */
@@ -64,6 +64,10 @@ extern "C" {
                                         (whole-array parity with the reference);
                                         default: only the consumed window
                                         cache_free[T - A, T) is written */
+#define CBTM_POOL_STAGED_LAUNCHES 2u /* one kernel launch per pipeline stage instead of
+                                        the persistent cooperative frame kernel (per-stage
+                                        profiling; automatic where cooperative launch is
+                                        unavailable) */
 
 /* stats layout written by cbtm_update to cbtm_pool.stats (int64) */
 enum {
@@ -78,7 +82,12 @@ enum {
     CBTM_STAT_RESERVED = 8,  /* T: slots reserved by admitted commands   */
     CBTM_STAT_ALLOCATED = 9, /* A: slots actually allocated              */
     CBTM_STAT_POISON = 10,   /* fresh pointers resolved to the poison -2 */
-    CBTM_STAT_FRAME = 11     /* frames applied to this pool so far       */
+    CBTM_STAT_FRAME = 11,    /* frames applied to this pool so far       */
+    /* words 16..24: device time of each phase of the frame in ns (persistent
+     * frame kernel only; 0 on the staged path): index, classify, admit, scatter,
+     * agree, alloc_scan, reserve, apply, sum_reduce -- cf. UpdateStats.stage_times_us */
+    CBTM_STAT_PHASE_NS = 16,
+    CBTM_STAT_PHASES = 9
 };
 
 /* One bisector pool == the reference's TriangulationState (state.py:32-55).

@@ -17,11 +17,14 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcbtm.so")
 
 PRM_WORDS = 23
-STATS_WORDS = 16
+STATS_WORDS = 32
+STAT_PHASE_NS = 16
+PHASE_NAMES = ("index", "classify", "admit", "scatter", "agree", "alloc_scan", "reserve", "apply", "sum_reduce")
 MIN_DEPTH = 1
 MAX_DEPTH_ABI = 30
 
 POOL_FULL_FREE_CACHE = 1
+POOL_STAGED_LAUNCHES = 2
 
 VERDICT_CONST, VERDICT_UNIFORM, VERDICT_LOD, VERDICT_EXPLICIT = 0, 1, 2, 3
 

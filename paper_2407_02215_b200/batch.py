@@ -55,7 +55,7 @@ def run_planet_batch(sequences, frames_params, world: int = 1, rank: int = 0,
     workloads.LodSequence objects, ``frames_params[p]`` is float64[frames, 23].
     Planets of one rank are interleaved frame by frame on the same stream (each
     frame is a fixed chain of launches), which keeps the GPU fed while any one
-    planet's chain is latency bound.  Returns (states, int64[owned, frames, 16])."""
+    planet's chain is latency bound.  Returns (states, int64[owned, frames, STATS_WORDS])."""
     from . import _lib
     from .pipeline import ParallelEngine
     from .state import initialize

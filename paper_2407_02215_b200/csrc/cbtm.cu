@@ -68,7 +68,7 @@ int reduce_launch(const uint64_t *bits, uint32_t *counters, int depth, unsigned 
     return launch_status();
 }
 
-const ReducePublish kNoPublish = {nullptr, nullptr, nullptr, nullptr};
+const ReducePublish kNoPublish = {nullptr, nullptr, nullptr, nullptr, nullptr};
 
 int check_pool(const cbtm_pool *p, bool need_ws)
 {
@@ -129,8 +129,8 @@ int index_launch(const cbtm_pool *pool, cudaStream_t st)
     return launch_status();
 }
 
-// stages 3-9 for a prepared FrameArgs
-int finish_launch(const FrameArgs &a, int64_t *stats_seq, cudaStream_t st)
+// stages 3-9, one kernel per phase (staged path)
+int finish_staged(const FrameArgs &a, int64_t *stats_seq, cudaStream_t st)
 {
     const unsigned grid = frame_grid(a.pool.depth);
     k_classify<<<grid, CHUNK, 0, st>>>(a, nullptr);
@@ -140,11 +140,43 @@ int finish_launch(const FrameArgs &a, int64_t *stats_seq, cudaStream_t st)
     k_alloc_scan<<<1, ADMIT_THREADS, 0, st>>>(a);
     k_reserve<<<grid, CHUNK, 0, st>>>(a);
     k_apply<<<grid, CHUNK, 0, st>>>(a);
-    int rc = launch_status();
+    const int rc = launch_status();
     if (rc) return rc;
-    const ReducePublish pub = {a.ws.ctl->stats, a.pool.stats, stats_seq, &a.ws.ctl->seq_frame};
+    const ReducePublish pub = {a.ws.ctl->stats, a.pool.stats, stats_seq, &a.ws.ctl->seq_frame, nullptr};
     return reduce_launch(a.pool.bits, a.pool.counters, a.pool.depth, a.ws.ticket, pub, st);
 }
+
+// Co-resident grid of the persistent frame kernel (0: cooperative launch unavailable)
+unsigned persistent_grid(int depth)
+{
+    static int ctas_per_sm = -1;
+    if (ctas_per_sm < 0) {
+        int dev = 0, coop = 0, per_sm = 0;
+        ctas_per_sm = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) == cudaSuccess && coop &&
+            cudaFuncSetAttribute(k_frames, cudaFuncAttributeMaxDynamicSharedMemorySize, FRAMES_DYN_SMEM) ==
+                cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_frames, CHUNK, FRAMES_DYN_SMEM) ==
+                cudaSuccess)
+            ctas_per_sm = per_sm > 2 ? 2 : per_sm;
+        (void)cudaGetLastError();
+    }
+    if (ctas_per_sm <= 0) return 0;
+    const uint64_t want = (((uint64_t)1 << depth) + CHUNK - 1) / CHUNK; // tiny pools: fewer CTAs, cheaper barriers
+    const uint64_t cap = (uint64_t)sm_count() * ctas_per_sm;
+    return (unsigned)(want < cap ? want : cap);
+}
+
+// n_frames full updates (optionally without the index phase) in one cooperative launch
+int frames_launch(FrameArgs &a, int n_frames, int64_t *stats_seq, int do_index, unsigned grid, cudaStream_t st)
+{
+    void *args[] = {(void *)&a, (void *)&n_frames, (void *)&stats_seq, (void *)&do_index};
+    return status(cudaLaunchCooperativeKernel((const void *)k_frames, dim3(grid), dim3(CHUNK), args,
+                                              FRAMES_DYN_SMEM, st));
+}
+
+inline bool staged(const cbtm_pool *pool) { return (pool->flags & CBTM_POOL_STAGED_LAUNCHES) != 0; }
 
 } // namespace
 
@@ -294,14 +326,25 @@ int cbtm_update_finish(const cbtm_pool *pool, const cbtm_verdict *verdict, uintp
     FrameArgs a;
     rc = fill_args(pool, verdict, &a);
     if (rc) return rc;
-    return finish_launch(a, nullptr, as_stream(stream));
+    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth);
+    if (!grid) return finish_staged(a, nullptr, as_stream(stream));
+    return frames_launch(a, 1, nullptr, 0, grid, as_stream(stream));
 }
 
 int cbtm_update(const cbtm_pool *pool, const cbtm_verdict *verdict, uintptr_t stream)
 {
-    const int rc = cbtm_update_begin(pool, stream);
+    int rc = check_pool(pool, true);
     if (rc) return rc;
-    return cbtm_update_finish(pool, verdict, stream);
+    if (!verdict) return CBTM_E_NULL;
+    FrameArgs a;
+    rc = fill_args(pool, verdict, &a);
+    if (rc) return rc;
+    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth);
+    if (!grid) {
+        rc = index_launch(pool, as_stream(stream));
+        return rc ? rc : finish_staged(a, nullptr, as_stream(stream));
+    }
+    return frames_launch(a, 1, nullptr, 1, grid, as_stream(stream));
 }
 
 int cbtm_run_lod_sequence(const cbtm_pool *pool, const double *root_tris, const double *prm_host,
@@ -322,6 +365,7 @@ int cbtm_run_lod_sequence(const cbtm_pool *pool, const double *root_tris, const 
     rc = fill_args(pool, &v, &a);
     if (rc) return rc;
     a.use_prm_seq = 1;
+    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth);
     for (int32_t done = 0; done < n_frames;) {
         const int32_t batch = n_frames - done < MAX_SEQ_FRAMES ? n_frames - done : MAX_SEQ_FRAMES;
         rc = status(cudaMemcpyAsync(a.ws.prm_seq, prm_host + (size_t)CBTM_PRM_WORDS * done,
@@ -330,11 +374,16 @@ int cbtm_run_lod_sequence(const cbtm_pool *pool, const double *root_tris, const 
         rc = status(cudaMemsetAsync(&a.ws.ctl->seq_frame, 0, sizeof(uint32_t), st));
         if (rc) return rc;
         int64_t *so = stats_out ? stats_out + (size_t)CBTM_STATS_WORDS * done : nullptr;
-        for (int32_t f = 0; f < batch; ++f) {
-            rc = index_launch(pool, st);
+        if (grid) {
+            rc = frames_launch(a, batch, so, 1, grid, st); // the whole batch in one launch
             if (rc) return rc;
-            rc = finish_launch(a, so, st);
-            if (rc) return rc;
+        } else {
+            for (int32_t f = 0; f < batch; ++f) {
+                rc = index_launch(pool, st);
+                if (rc) return rc;
+                rc = finish_staged(a, so, st);
+                if (rc) return rc;
+            }
         }
         done += batch;
     }

@@ -36,7 +36,15 @@ struct ReducePublish {
     int64_t *pool_stats; // cbtm_pool::stats
     int64_t *stats_seq;  // per-frame rows of a sequence run
     uint32_t *seq_frame; // Control::seq_frame
+    const unsigned long long *phase_t; // Control::phase_t (persistent kernel) or NULL
 };
+
+__device__ __forceinline__ unsigned long long global_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ void publish_frame(const ReducePublish &pub, uint32_t live_after, int tid)
 {
@@ -47,6 +55,15 @@ __device__ __forceinline__ void publish_frame(const ReducePublish &pub, uint32_t
         if (tid == CBTM_STAT_FRAME) {
             v += 1;
             pub.ctl_stats[tid] = v;
+        }
+        if (tid >= CBTM_STAT_PHASE_NS && tid < CBTM_STAT_PHASE_NS + CBTM_STAT_PHASES) {
+            v = 0;
+            if (pub.phase_t) { // stamp k = start of phase k; the reduction ends now
+                const int k = tid - CBTM_STAT_PHASE_NS;
+                const unsigned long long t0 = pub.phase_t[k];
+                const unsigned long long t1 = k + 1 < CBTM_STAT_PHASES ? pub.phase_t[k + 1] : global_ns();
+                v = t1 > t0 ? (int64_t)(t1 - t0) : 0;
+            }
         }
         if (pub.pool_stats) pub.pool_stats[tid] = v;
         if (pub.stats_seq) pub.stats_seq[(size_t)CBTM_STATS_WORDS * (*pub.seq_frame) + tid] = v;
@@ -95,48 +112,68 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
                  : "memory");
 }
 
-__global__ void __launch_bounds__(RED_THREADS)
-k_sum_reduce(const uint8_t *__restrict__ bits, uint32_t *__restrict__ counters, int lc,
-             uint64_t total_bytes, uint32_t n_tiles, int stages, unsigned *ticket,
-             const ReducePublish pub)
-{
-    extern __shared__ __align__(128) uint8_t ring[]; // stages x 16 KB
-    __shared__ __align__(8) uint64_t full[RED_MAX_STAGES];
-    __shared__ uint32_t wroot[2][RED_THREADS / 32];
-    __shared__ bool is_last;
+// Per-CTA state of the TMA ring that survives across frames of a persistent
+// kernel: barriers are initialised once, `iter` counts the tiles this CTA has
+// pushed through the ring so far (stage = iter % stages, parity = iter / stages).
+struct ReduceRing {
+    uint8_t *ring;   // stages x 16 KB of shared memory (also the upper-tree heap)
+    uint64_t *full;  // RED_MAX_STAGES mbarriers
+    uint32_t (*wroot)[RED_THREADS / 32]; // [2][8]
+    bool *is_last;
+    int stages;
+    uint32_t iter;
+};
 
+__device__ __forceinline__ void reduce_ring_init(ReduceRing &rr)
+{
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < rr.stages; ++s) mbar_init(&rr.full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    rr.iter = 0;
+    __syncthreads();
+}
+
+// One full sum reduction by the CTAs (bid of nb).  All nb CTAs must call it.
+__device__ __forceinline__ void reduce_phase(const uint8_t *bits, uint32_t *counters, int lc,
+                                             uint64_t total_bytes, uint32_t n_tiles, unsigned *ticket,
+                                             const ReducePublish &pub, ReduceRing &rr, uint32_t bid,
+                                             uint32_t nb)
+{
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    // tiles are dealt round-robin (tile = blockIdx.x + k * gridDim.x): at any moment the
-    // CTAs read one contiguous window of the bitfield, which keeps DRAM rows open
-    const uint32_t tile0 = blockIdx.x, tile_step = gridDim.x;
-    const uint32_t my_tiles = tile0 < n_tiles ? (n_tiles - tile0 + tile_step - 1) / tile_step : 0u;
+    const uint32_t stages = (uint32_t)rr.stages;
+    // tiles are dealt round-robin (tile = bid + k * nb): at any moment the CTAs read
+    // one contiguous window of the bitfield, which keeps DRAM rows open
+    const uint32_t my_tiles = bid < n_tiles ? (n_tiles - bid + nb - 1) / nb : 0u;
+    const uint32_t it0 = rr.iter;
 
     auto tile_bytes = [&](uint32_t tile) -> uint32_t {
         const uint64_t left = total_bytes - (uint64_t)tile * RED_TILE_BYTES;
         return left < RED_TILE_BYTES ? (uint32_t)left : (uint32_t)RED_TILE_BYTES;
     };
-    auto issue = [&](uint32_t tile, int stage) {
+    auto issue = [&](uint32_t tile, uint32_t it) {
+        const uint32_t stage = it % stages;
         const uint32_t bytes = tile_bytes(tile);
-        mbar_expect_tx(&full[stage], bytes);
-        bulk_load(ring + (size_t)stage * RED_TILE_BYTES, bits + (size_t)tile * RED_TILE_BYTES, bytes,
-                  &full[stage]);
+        mbar_expect_tx(&rr.full[stage], bytes);
+        bulk_load(rr.ring + (size_t)stage * RED_TILE_BYTES, bits + (size_t)tile * RED_TILE_BYTES, bytes,
+                  &rr.full[stage]);
     };
 
     if (t == 0) {
-        for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // the ring may have been written through the generic proxy (index staging,
+        // upper-tree heap) since the last bulk copy
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (uint32_t k = 0; k < stages && k < my_tiles; ++k) issue(bid + k * nb, it0 + k);
     }
-    __syncthreads();
-    if (t == 0)
-        for (uint32_t k = 0; k < (uint32_t)stages && k < my_tiles; ++k) issue(tile0 + k * tile_step, (int)k);
 
     for (uint32_t k = 0; k < my_tiles; ++k) {
-        const uint32_t tile = tile0 + k * tile_step;
-        const int stage = (int)(k % (uint32_t)stages);
-        mbar_wait(&full[stage], (k / (uint32_t)stages) & 1u);
+        const uint32_t tile = bid + k * nb;
+        const uint32_t it = it0 + k;
+        const uint32_t stage = it % stages;
+        mbar_wait(&rr.full[stage], (it / stages) & 1u);
 
         // my 64 bytes of the tile; the rotation keeps the four LDS.128 conflict free
-        const uint4 *mine = reinterpret_cast<const uint4 *>(ring + (size_t)stage * RED_TILE_BYTES) + t * 4;
+        const uint4 *mine = reinterpret_cast<const uint4 *>(rr.ring + (size_t)stage * RED_TILE_BYTES) + t * 4;
         uint32_t c = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) c += popc128(mine[(j + (lane >> 1)) & 3]);
@@ -163,11 +200,11 @@ k_sum_reduce(const uint8_t *__restrict__ bits, uint32_t *__restrict__ counters, 
             val = l4, lvl = lc - 4, pos = tile * 8 + warp;
         }
         if (lvl >= 0 && pos < (1u << lvl)) counters[(1u << lvl) + pos] = val;
-        if (lane == 0) wroot[k & 1][warp] = l4;
+        if (lane == 0) rr.wroot[k & 1][warp] = l4;
         __syncthreads(); // stage consumed by everyone; warp roots visible
-        if (t == 0 && k + (uint32_t)stages < my_tiles) issue(tile + (uint32_t)stages * tile_step, stage);
+        if (t == 0 && k + stages < my_tiles) issue(tile + stages * nb, it + stages);
         if (warp == 0 && lane < 7) { // levels lc-5 (4 nodes), lc-6 (2), lc-7 (tile root)
-            const uint32_t *w = wroot[k & 1];
+            const uint32_t *w = rr.wroot[k & 1];
             uint32_t v2, p2;
             int l5;
             if (lane < 4) {
@@ -181,10 +218,14 @@ k_sum_reduce(const uint8_t *__restrict__ bits, uint32_t *__restrict__ counters, 
             if (l5 >= 0 && p2 < (1u << l5)) counters[(1u << l5) + p2] = v2;
         }
     }
+    rr.iter = it0 + my_tiles;
 
-    if (n_tiles == 1) { // the single tile's subtree is the whole tree
-        const uint32_t *w = wroot[0];
-        publish_frame(pub, w[0] + w[1] + w[2] + w[3] + w[4] + w[5] + w[6] + w[7], t);
+    if (n_tiles == 1) { // the single tile's subtree is the whole tree (CTA 0 owns it)
+        if (bid == 0) {
+            const uint32_t *w = rr.wroot[0];
+            publish_frame(pub, w[0] + w[1] + w[2] + w[3] + w[4] + w[5] + w[6] + w[7], t);
+        }
+        __syncthreads();
         return;
     }
 
@@ -192,18 +233,18 @@ k_sum_reduce(const uint8_t *__restrict__ bits, uint32_t *__restrict__ counters, 
     __syncthreads();
     if (t == 0) {
         __threadfence();
-        is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        *rr.is_last = atomicAdd(ticket, 1u) == nb - 1;
     }
     __syncthreads();
-    if (!is_last) return;
+    if (!*rr.is_last) return;
     __threadfence();
 
     // Upper tree as a binary heap in the (now idle) ring: coalesced L2 loads of the
     // tile roots, issued eight at a time per thread so they overlap; log2(cnt)
     // levels in shared memory; one coalesced copy-out of all internal nodes.
     // (Walking the levels through L2 instead costs a round trip per level.)
-    uint32_t *heap = reinterpret_cast<uint32_t *>(ring); // 2 * cnt words <= stages * 16 KB
-    const uint32_t cnt = n_tiles;                        // power of two, 2 .. 8192
+    uint32_t *heap = reinterpret_cast<uint32_t *>(rr.ring); // 2 * cnt words <= stages * 16 KB
+    const uint32_t cnt = n_tiles;                           // power of two, 2 .. 8192
     for (uint32_t base = 0; base < cnt; base += 8 * RED_THREADS) {
         uint32_t r[8];
 #pragma unroll
@@ -225,6 +266,20 @@ k_sum_reduce(const uint8_t *__restrict__ bits, uint32_t *__restrict__ counters, 
     for (uint32_t i = 1 + t; i < cnt; i += RED_THREADS) counters[i] = heap[i];
     if (t == 0) *ticket = 0;
     publish_frame(pub, heap[1], t);
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(RED_THREADS)
+k_sum_reduce(const uint8_t *bits, uint32_t *counters, int lc, uint64_t total_bytes, uint32_t n_tiles,
+             int stages, unsigned *ticket, const ReducePublish pub)
+{
+    extern __shared__ __align__(128) uint8_t dyn_smem[]; // stages x 16 KB
+    __shared__ __align__(8) uint64_t full[RED_MAX_STAGES];
+    __shared__ uint32_t wroot[2][RED_THREADS / 32];
+    __shared__ bool is_last;
+    ReduceRing rr{dyn_smem, full, wroot, &is_last, stages, 0};
+    reduce_ring_init(rr);
+    reduce_phase(bits, counters, lc, total_bytes, n_tiles, ticket, pub, rr, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -233,15 +288,14 @@ k_sum_reduce(const uint8_t *__restrict__ bits, uint32_t *__restrict__ counters, 
 // block.
 // ---------------------------------------------------------------------------
 template <bool ONES>
-__device__ __forceinline__ int32_t cbt_find(const uint64_t *__restrict__ bits,
-                                            const uint32_t *__restrict__ counters,
+__device__ __forceinline__ int32_t cbt_find(const uint64_t *bits, const uint32_t *counters,
                                             const Geo &g, uint32_t rank)
 {
     uint32_t node = 1;
     uint32_t half = (uint32_t)(g.n >> 1); // slots under a child of the current node
     for (int l = 0; l < g.lc; ++l) {
         node <<= 1;
-        const uint32_t ones = __ldg(&counters[node]);
+        const uint32_t ones = counters[node];
         const uint32_t left = ONES ? ones : half - ones;
         if (rank >= left) {
             rank -= left;
@@ -253,7 +307,7 @@ __device__ __forceinline__ int32_t cbt_find(const uint64_t *__restrict__ bits,
     const uint64_t *line = bits + (size_t)block * 16;
     const int words = g.span >= 64 ? (int)(g.span >> 6) : 1;
     for (int w = 0; w < words; ++w) {
-        uint64_t x = __ldg(&line[w]);
+        uint64_t x = line[w];
         if (!ONES) {
             x = ~x;
             if (g.span < 64) x &= (((uint64_t)1 << g.span) - 1);
@@ -297,18 +351,19 @@ constexpr int IDX_WARPS = 8;
 // the copy-out reads 32 consecutive elements, which stay conflict free.
 __device__ __forceinline__ uint32_t stage_at(uint32_t i) { return i ^ ((i >> 5) & 31u); }
 
-__global__ void __launch_bounds__(IDX_WARPS * 32)
-k_index(const uint32_t *__restrict__ bits32, const uint32_t *__restrict__ counters, int depth,
-        int32_t *__restrict__ cache_live, int32_t *__restrict__ cache_free,
-        uint32_t *__restrict__ dispatch)
+// `stage` is IDX_WARPS x 1024 words of shared memory.  Plain (coherent) loads
+// only: inside the persistent frame kernel the bitfield and the counters were
+// written earlier in the same launch.
+__device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32_t *counters, int depth,
+                                            int32_t *cache_live, int32_t *cache_free, uint32_t *dispatch,
+                                            int32_t (*stage)[1024], uint32_t bid, uint32_t nb)
 {
-    __shared__ int32_t stage[IDX_WARPS][1024];
     const Geo g = make_geo(depth);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t gwarp = blockIdx.x * IDX_WARPS + warp;
-    const uint32_t nwarps = gridDim.x * IDX_WARPS;
+    const uint32_t gwarp = bid * IDX_WARPS + warp;
+    const uint32_t nwarps = nb * IDX_WARPS;
 
-    if (dispatch && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (dispatch && bid == 0 && threadIdx.x == 0) {
         const uint32_t n = counters[1];
         dispatch[0] = (n + CHUNK - 1) / CHUNK;
         dispatch[1] = 1;
@@ -317,60 +372,78 @@ k_index(const uint32_t *__restrict__ bits32, const uint32_t *__restrict__ counte
     }
 
     int32_t *st = stage[warp];
-    for (uint32_t b = gwarp; b < g.nblocks; b += nwarps) {
-        const uint32_t cnt = __ldg(&counters[g.nblocks + b]);
-        if (cnt == 0 && !cache_free) continue;
+    // this warp owns leaf blocks gwarp + k * nwarps; lane k fetches the count of the
+    // k-th of them, so one round trip tells the warp which of its next 32 blocks
+    // hold anything (a sparse pool skips almost all of them)
+    for (uint32_t k0 = 0; gwarp + (uint64_t)k0 * nwarps < g.nblocks; k0 += 32) {
+        const uint64_t mine = gwarp + (uint64_t)(k0 + lane) * nwarps;
+        const uint32_t my_cnt = mine < g.nblocks ? counters[g.nblocks + mine] : 0u;
+        unsigned todo = __ballot_sync(FULL_MASK, mine < g.nblocks && (my_cnt != 0 || cache_free != nullptr));
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint32_t b = gwarp + (k0 + src) * nwarps;
+            const uint32_t cnt = __shfl_sync(FULL_MASK, my_cnt, src);
 
-        // ones before this block: left siblings along the root path
-        uint32_t part = 0;
-        if (lane >= 1 && lane <= g.lc) {
-            const uint32_t idx = b >> (g.lc - lane);
-            if (idx & 1) part = __ldg(&counters[(1u << lane) + idx - 1]);
-        }
-        const uint32_t ones_before = warp_sum(part);
-        const uint32_t zeros_before = b * g.span - ones_before;
-        const int32_t base = (int32_t)(b * g.span);
-        const uint32_t zcnt = g.span - cnt;
-
-        if (cnt == 0) { // all free
-            for (uint32_t i = lane; i < g.span; i += 32) cache_free[zeros_before + i] = base + (int32_t)i;
-            continue;
-        }
-        if (cnt == g.span) { // all live
-            for (uint32_t i = lane; i < g.span; i += 32) cache_live[ones_before + i] = base + (int32_t)i;
-            continue;
-        }
-
-        const uint32_t valid = g.span >= 1024 ? 32u
-                             : (lane * 32u >= g.span ? 0u : (g.span - lane * 32u >= 32u ? 32u : g.span - lane * 32u));
-        uint32_t w = valid ? bits32[(size_t)b * 32 + lane] : 0u;
-        const uint32_t vmask = valid == 32 ? 0xffffffffu : ((1u << valid) - 1u);
-        w &= vmask;
-        const uint32_t c = __popc(w);
-        const uint32_t incl = warp_inclusive_scan(c);
-        uint32_t o1 = incl - c;                     // set bits before this lane
-        uint32_t o0 = cnt + (lane * 32u > g.span ? g.span : lane * 32u) - o1; // staged after the ones
-        const int32_t lane_base = base + lane * 32;
-        uint32_t ones = w;
-        while (ones) {
-            const int k = __ffs(ones) - 1;
-            ones &= ones - 1;
-            st[stage_at(o1++)] = lane_base + k;
-        }
-        if (cache_free) {
-            uint32_t zeros = ~w & vmask;
-            while (zeros) {
-                const int k = __ffs(zeros) - 1;
-                zeros &= zeros - 1;
-                st[stage_at(o0++)] = lane_base + k;
+            // ones before this block: left siblings along the root path
+            uint32_t part = 0;
+            if (lane >= 1 && lane <= g.lc) {
+                const uint32_t idx = b >> (g.lc - lane);
+                if (idx & 1) part = counters[(1u << lane) + idx - 1];
             }
+            const uint32_t ones_before = warp_sum(part);
+            const uint32_t zeros_before = b * g.span - ones_before;
+            const int32_t base = (int32_t)(b * g.span);
+            const uint32_t zcnt = g.span - cnt;
+
+            if (cnt == 0) { // all free
+                for (uint32_t i = lane; i < g.span; i += 32) cache_free[zeros_before + i] = base + (int32_t)i;
+                continue;
+            }
+            if (cnt == g.span) { // all live
+                for (uint32_t i = lane; i < g.span; i += 32) cache_live[ones_before + i] = base + (int32_t)i;
+                continue;
+            }
+
+            const uint32_t valid = g.span >= 1024 ? 32u
+                                 : (lane * 32u >= g.span ? 0u : (g.span - lane * 32u >= 32u ? 32u : g.span - lane * 32u));
+            uint32_t w = valid ? bits32[(size_t)b * 32 + lane] : 0u;
+            const uint32_t vmask = valid == 32 ? 0xffffffffu : ((1u << valid) - 1u);
+            w &= vmask;
+            const uint32_t c = __popc(w);
+            const uint32_t incl = warp_inclusive_scan(c);
+            uint32_t o1 = incl - c;                     // set bits before this lane
+            uint32_t o0 = cnt + (lane * 32u > g.span ? g.span : lane * 32u) - o1; // staged after the ones
+            const int32_t lane_base = base + lane * 32;
+            uint32_t ones = w;
+            while (ones) {
+                const int k = __ffs(ones) - 1;
+                ones &= ones - 1;
+                st[stage_at(o1++)] = lane_base + k;
+            }
+            if (cache_free) {
+                uint32_t zeros = ~w & vmask;
+                while (zeros) {
+                    const int k = __ffs(zeros) - 1;
+                    zeros &= zeros - 1;
+                    st[stage_at(o0++)] = lane_base + k;
+                }
+            }
+            __syncwarp();
+            for (uint32_t i = lane; i < cnt; i += 32) cache_live[ones_before + i] = st[stage_at(i)];
+            if (cache_free)
+                for (uint32_t i = lane; i < zcnt; i += 32) cache_free[zeros_before + i] = st[stage_at(cnt + i)];
+            __syncwarp();
         }
-        __syncwarp();
-        for (uint32_t i = lane; i < cnt; i += 32) cache_live[ones_before + i] = st[stage_at(i)];
-        if (cache_free)
-            for (uint32_t i = lane; i < zcnt; i += 32) cache_free[zeros_before + i] = st[stage_at(cnt + i)];
-        __syncwarp();
     }
+}
+
+__global__ void __launch_bounds__(IDX_WARPS * 32)
+k_index(const uint32_t *bits32, const uint32_t *counters, int depth, int32_t *cache_live,
+        int32_t *cache_free, uint32_t *dispatch)
+{
+    __shared__ int32_t stage[IDX_WARPS][1024];
+    index_phase(bits32, counters, depth, cache_live, cache_free, dispatch, stage, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------

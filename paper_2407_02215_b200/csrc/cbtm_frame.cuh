@@ -16,10 +16,18 @@
 //              [T - incl_i, T - incl_i + n_alloc_i), incl = inclusive scan of
 //              n_alloc, T = total admitted reservation
 //
-// Launch order per frame (all on one stream, no host synchronisation):
-//   k_classify -> k_admit -> k_scatter -> k_agree -> k_alloc_scan -> k_reserve
-//   -> k_apply -> k_sum_reduce (its last CTA also publishes the frame's stats)
+// Phases of one frame, each a __device__ function over virtual CTA ids (bid of nb):
+//   index -> classify -> admit (1 CTA) -> scatter -> agree -> alloc_scan (1 CTA)
+//   -> reserve -> apply -> sum reduction (its last CTA also publishes the stats)
+// They run either as ONE persistent cooperative kernel (k_frames: phases
+// separated by grid barriers, any number of frames per launch -- a frame is
+// latency bound, so not paying a launch ramp and drain per phase is what
+// matters) or as one kernel per phase (k_<phase> wrappers: the staged path used
+// for the python-callable verdict source, for per-stage profiling and as the
+// fallback where cooperative launch is unavailable).
 #pragma once
+
+#include <cooperative_groups.h>
 
 #include "cbtm_cbt.cuh"
 #include "cbtm_classify.cuh"
@@ -27,8 +35,9 @@
 namespace cbtm {
 
 constexpr int TAIL_MAX = 96;
-constexpr int ADMIT_THREADS = 1024;
+constexpr int ADMIT_THREADS = 1024; // standalone single-CTA kernels; 256 inside k_frames
 constexpr int MAX_SEQ_FRAMES = 4096;
+constexpr int WIN_MAX = 4096;       // leaf blocks covered by the free-rank window table
 
 // device-resident control block of one pool (lives in the workspace)
 struct Control {
@@ -37,6 +46,9 @@ struct Control {
     int32_t tail_count;
     uint32_t seq_frame; // index into prm_seq for sequence runs
     int32_t tail_idx[TAIL_MAX];
+    uint32_t win_lo; // first leaf block of the free-rank window [T - A, T)
+    uint32_t win_n;  // leaf blocks in the window table (0: table not built, descend)
+    unsigned long long phase_t[CBTM_STAT_PHASES + 1]; // %globaltimer at the start of each phase
     int64_t stats[CBTM_STATS_WORDS];
 };
 
@@ -44,12 +56,14 @@ struct Workspace {
     uint8_t *need8;   // [N] by live rank: slots to reserve (0 = no command)
     uint8_t *mbits8;  // [N] by live rank: merge command bits of a merge request
     uint8_t *nalloc8; // [N] by live rank: slots actually allocated
-    uint8_t *flags8;  // [N] by slot: bit0 = member of an agreed merge
+    int32_t *merge_ref; // [N] by slot: -1, or for a member of an agreed merge 2 * owner slot + (1 if the
+                        // member sits in the pair opposite to the owner's, i.e. its parent is reserved[owner][1])
     uint32_t *chunk_need;
     uint64_t *chunk_need_off;
     uint32_t *chunk_alloc;
     uint64_t *chunk_alloc_off;
     uint8_t *chunk_minneed;
+    uint32_t *win_prefix; // [WIN_MAX + 1] free ranks before each leaf block of the window
     Control *ctl;
     double *prm_seq;  // [MAX_SEQ_FRAMES * 23]
     unsigned *ticket; // first word of the workspace: k_sum_reduce's CTA ticket
@@ -75,12 +89,13 @@ inline size_t carve_workspace(void *base, int depth, Workspace *ws)
     w.need8 = (uint8_t *)take(N);
     w.mbits8 = (uint8_t *)take(N);
     w.nalloc8 = (uint8_t *)take(N);
-    w.flags8 = (uint8_t *)take(N);
+    w.merge_ref = (int32_t *)take(4 * N);
     w.chunk_need = (uint32_t *)take(4 * nch);
     w.chunk_need_off = (uint64_t *)take(8 * nch);
     w.chunk_alloc = (uint32_t *)take(4 * nch);
     w.chunk_alloc_off = (uint64_t *)take(8 * nch);
     w.chunk_minneed = (uint8_t *)take(nch);
+    w.win_prefix = (uint32_t *)take(4 * (WIN_MAX + 1));
     if (ws) *ws = w;
     return off;
 }
@@ -134,39 +149,11 @@ __device__ __forceinline__ bool wants_only_merge(uint32_t cmd)
     return !(cmd & CBTM_CMD_SPLIT_MASK) && (cmd & CBTM_CMD_MERGE);
 }
 
-// reserved slot of the parent that replaces merging member m (kernels.py:159-180)
-__device__ __forceinline__ int32_t merge_parent_slot(const cbtm_pool &p, int32_t m)
-{
-    const uint64_t jm = p.ids[m];
-    const MergeCfg c = merge_config(p, m, jm);
-    int32_t owner = m;
-    uint64_t best = jm;
-    const uint64_t js = p.ids[c.sib];
-    if (js < best) {
-        best = js;
-        owner = c.sib;
-    }
-    if (c.kind == 2) {
-        const uint64_t jo = p.ids[c.oth], j4 = p.ids[c.j4];
-        if (jo < best) {
-            best = jo;
-            owner = c.oth;
-        }
-        if (j4 < best) {
-            best = j4;
-            owner = c.j4;
-        }
-    }
-    if (c.kind == 1 || (jm >> 1) == (best >> 1)) return p.reserved[4 * (size_t)owner];
-    return p.reserved[4 * (size_t)owner + 1];
-}
-
 // ---------------------------------------------------------------------------
 // stage 3 + 4a: reset commands, evaluate verdicts, compute each rank's
 // reservation need (3d+4 for a split, 2 for a valid merge, 0 otherwise).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(CHUNK)
-k_classify(const __grid_constant__ FrameArgs a, int8_t *__restrict__ verdict_out)
+__device__ __forceinline__ void phase_classify(const FrameArgs &a, int8_t *verdict_out, uint32_t bid, uint32_t nb)
 {
     __shared__ double prm[CBTM_PRM_WORDS];
     __shared__ uint32_t wsum[CHUNK / 32], wmin[CHUNK / 32];
@@ -182,7 +169,7 @@ k_classify(const __grid_constant__ FrameArgs a, int8_t *__restrict__ verdict_out
         __syncthreads();
     }
 
-    for (uint32_t chunk = blockIdx.x; chunk < nch; chunk += gridDim.x) {
+    for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
         const uint32_t i = chunk * CHUNK + tid;
         uint32_t need = 0, mbits = 0;
         if (i < n) {
@@ -248,8 +235,8 @@ k_classify(const __grid_constant__ FrameArgs a, int8_t *__restrict__ verdict_out
 // stage 4b (one CTA): admission.  Scans the per-chunk needs, locates the first
 // overflowing rank i0 and runs the first-fit tail walk.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(ADMIT_THREADS)
-k_admit(const __grid_constant__ FrameArgs a)
+template <int NT>
+__device__ __forceinline__ void phase_admit(const FrameArgs &a)
 {
     __shared__ uint32_t scratch[32];
     __shared__ uint32_t s_warpmin[32];
@@ -265,7 +252,7 @@ k_admit(const __grid_constant__ FrameArgs a)
     const uint64_t F = ((uint64_t)1 << p.depth) - n;
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
 
-    if (tid < CBTM_STATS_WORDS && tid != CBTM_STAT_FRAME) ctl->stats[tid] = 0;
+    if (tid < CBTM_STAT_PHASE_NS && tid != CBTM_STAT_FRAME) ctl->stats[tid] = 0;
     if (tid == 0) {
         s_carry = 0;
         s_c0 = nch;
@@ -273,11 +260,11 @@ k_admit(const __grid_constant__ FrameArgs a)
     __syncthreads();
 
     // ---- exclusive scan of the chunk needs, first overflowing chunk ----
-    for (uint32_t base = 0; base < nch; base += ADMIT_THREADS) {
+    for (uint32_t base = 0; base < nch; base += NT) {
         const uint32_t c = base + tid;
         const uint32_t v = c < nch ? a.ws.chunk_need[c] : 0;
         uint32_t total;
-        const uint32_t incl = block_inclusive_scan<ADMIT_THREADS>(v, scratch, &total);
+        const uint32_t incl = block_inclusive_scan<NT>(v, scratch, &total);
         const unsigned long long carry = s_carry;
         if (c < nch) {
             const unsigned long long off = carry + incl - v;
@@ -309,7 +296,7 @@ k_admit(const __grid_constant__ FrameArgs a)
         const uint32_t i = c0 * CHUNK + tid;
         const uint32_t v = (tid < CHUNK && i < n) ? a.ws.need8[i] : 0;
         uint32_t total;
-        const uint32_t incl = block_inclusive_scan<ADMIT_THREADS>(v, scratch, &total);
+        const uint32_t incl = block_inclusive_scan<NT>(v, scratch, &total);
         const unsigned long long off = a.ws.chunk_need_off[c0];
         if (tid == 0) s_found = 0xffffffffu;
         __syncthreads();
@@ -359,7 +346,7 @@ k_admit(const __grid_constant__ FrameArgs a)
         if (room < 2) break;
         if (tid == 0) s_next = nch;
         __syncthreads();
-        for (uint32_t base = c + 1; base < nch; base += ADMIT_THREADS) {
+        for (uint32_t base = c + 1; base < nch; base += NT) {
             const uint32_t cc = base + tid;
             const bool ok = cc < nch && a.ws.chunk_minneed[cc] <= room;
             const unsigned b = __ballot_sync(FULL_MASK, ok);
@@ -367,7 +354,7 @@ k_admit(const __grid_constant__ FrameArgs a)
             __syncthreads();
             if (tid == 0) {
                 uint32_t m = 0xffffffffu;
-                for (int w = 0; w < ADMIT_THREADS / 32; ++w) m = min(m, s_warpmin[w]);
+                for (int w = 0; w < NT / 32; ++w) m = min(m, s_warpmin[w]);
                 if (m != 0xffffffffu) s_next = m;
             }
             __syncthreads();
@@ -399,29 +386,38 @@ k_admit(const __grid_constant__ FrameArgs a)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void walk_split_chain(const cbtm_pool &p, int32_t s)
 {
+    // Pointer fields do not change during this phase, so the twin's operators
+    // are fetched while the atomic on `cur` is still in flight, and the twin's
+    // twin doubles as the next hop's twin: one dependent round trip per hop.
     int32_t cur = s;
+    int32_t t = p.twins[cur];
     for (int hops = 0;;) {
+        int32_t t_twin = -1, t_next = -1, t_prev = -1;
+        if (t >= 0) {
+            t_twin = p.twins[t];
+            t_next = p.nexts[t];
+            t_prev = p.prevs[t];
+        }
         const uint32_t before = atomicOr(&p.commands[cur], CBTM_CMD_SPLIT_T);
         if (before & CBTM_CMD_SPLIT_T) break; // another walker owns the rest of the chain
-        const int32_t t = p.twins[cur];
         if (t < 0) break;
-        if (p.twins[t] == cur) {
+        if (t_twin == cur) {
             atomicOr(&p.commands[t], CBTM_CMD_SPLIT_T);
             break;
         }
-        if (p.nexts[t] == cur)
+        if (t_next == cur)
             atomicOr(&p.commands[t], CBTM_CMD_SPLIT_N);
-        else if (p.prevs[t] == cur)
+        else if (t_prev == cur)
             atomicOr(&p.commands[t], CBTM_CMD_SPLIT_P);
         else
             break;
         cur = t;
+        t = t_twin;
         if (++hops > 70) break;
     }
 }
 
-__global__ void __launch_bounds__(CHUNK)
-k_scatter(const __grid_constant__ FrameArgs a)
+__device__ __forceinline__ void phase_scatter(const FrameArgs &a, uint32_t bid, uint32_t nb)
 {
     __shared__ int32_t tail[TAIL_MAX];
     __shared__ uint32_t oom[2];
@@ -437,7 +433,7 @@ k_scatter(const __grid_constant__ FrameArgs a)
     __syncthreads();
 
     uint32_t my_oom_s = 0, my_oom_m = 0;
-    for (uint32_t chunk = blockIdx.x; chunk < nch; chunk += gridDim.x) {
+    for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
         const uint32_t i = chunk * CHUNK + tid;
         if (i >= n) continue;
         const uint32_t need = a.ws.need8[i];
@@ -468,36 +464,50 @@ k_scatter(const __grid_constant__ FrameArgs a)
 
 // ---------------------------------------------------------------------------
 // stage 5a: with all commands final, snapshot the merge agreement of every
-// live slot (flags8) and count each rank's allocations (kernels.py:347-368).
+// live slot (merge_ref: owner and pair of every agreed-merge member) and count
+// each rank's allocations (kernels.py:347-368).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(CHUNK)
-k_agree(const __grid_constant__ FrameArgs a)
+__device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t bid, uint32_t nb)
 {
     __shared__ uint32_t wsum[CHUNK / 32];
     const cbtm_pool &p = a.pool;
     const uint32_t n = (uint32_t)a.ws.ctl->n;
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (uint32_t chunk = blockIdx.x; chunk < nch; chunk += gridDim.x) {
+    for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
         const uint32_t i = chunk * CHUNK + tid;
         uint32_t na = 0;
         if (i < n) {
             const int32_t s = p.cache_live[i];
             const uint32_t cmd = p.commands[s];
             const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
-            uint32_t agreed = 0;
+            int32_t ref = -1;
             if (sm) {
                 na = 2 + ((sm >> 1) & 1) + ((sm >> 2) & 1);
             } else if (cmd & CBTM_CMD_MERGE) {
-                const MergeCfg c = merge_config(p, s, p.ids[s]);
+                const uint64_t js = p.ids[s];
+                const MergeCfg c = merge_config(p, s, js);
+                bool agreed = false;
                 if (c.kind) {
                     agreed = wants_only_merge(p.commands[c.sib]);
                     if (agreed && c.kind == 2)
                         agreed = wants_only_merge(p.commands[c.oth]) && wants_only_merge(p.commands[c.j4]);
                 }
-                if (agreed && (cmd & CBTM_CMD_OWNER)) na = (cmd & CBTM_CMD_QUAD) ? 2 : 1;
+                if (agreed) { // owner = member with the smallest id (kernels.py:159-180)
+                    int32_t owner = s;
+                    uint64_t best = js;
+                    const uint64_t jb = p.ids[c.sib];
+                    if (jb < best) best = jb, owner = c.sib;
+                    if (c.kind == 2) {
+                        const uint64_t jo = p.ids[c.oth], j4 = p.ids[c.j4];
+                        if (jo < best) best = jo, owner = c.oth;
+                        if (j4 < best) best = j4, owner = c.j4;
+                    }
+                    ref = 2 * owner + ((c.kind == 2 && (js >> 1) != (best >> 1)) ? 1 : 0);
+                    if (cmd & CBTM_CMD_OWNER) na = (cmd & CBTM_CMD_QUAD) ? 2 : 1;
+                }
             }
-            a.ws.flags8[s] = (uint8_t)agreed;
+            a.ws.merge_ref[s] = ref;
             a.ws.nalloc8[i] = (uint8_t)na;
         }
         const uint32_t sum = warp_sum(na);
@@ -513,34 +523,106 @@ k_agree(const __grid_constant__ FrameArgs a)
     }
 }
 
-// stage 5b (one CTA): exclusive scan of the per-chunk allocation counts
-__global__ void __launch_bounds__(ADMIT_THREADS)
-k_alloc_scan(const __grid_constant__ FrameArgs a)
+// Leaf block holding the free (unset) rank `rank` and the number of free slots
+// before that block.  One warp descends the counter heap five levels per step:
+// the 32 descendants of a node five levels down are contiguous in the heap, so
+// a step is one coalesced load, a warp scan and a ballot (4 round trips for
+// D = 26 instead of 16 dependent loads).
+__device__ __forceinline__ void warp_find_free_block(const uint32_t *counters, const Geo &g, uint32_t rank,
+                                                     uint32_t &block, uint32_t &free_before)
+{
+    const int lane = threadIdx.x & 31;
+    uint32_t idx = 0, before = 0; // node idx of level l
+    int l = 0;
+    while (l < g.lc) {
+        const int s = g.lc - l < 5 ? g.lc - l : 5;
+        const uint32_t fan = 1u << s;
+        const uint32_t child_span = (uint32_t)(g.n >> (l + s));
+        uint32_t z = 0;
+        if ((uint32_t)lane < fan) z = child_span - counters[(1u << (l + s)) + (idx << s) + lane];
+        const uint32_t incl = warp_inclusive_scan(z);
+        const unsigned hit = __ballot_sync(FULL_MASK, (uint32_t)lane < fan && incl > rank);
+        const int child = hit ? __ffs(hit) - 1 : (int)fan - 1;
+        const uint32_t excl = __shfl_sync(FULL_MASK, incl - z, child);
+        rank -= excl;
+        before += excl;
+        idx = (idx << s) + child;
+        l += s;
+    }
+    block = idx;
+    free_before = before;
+}
+
+// stage 5b (one CTA): exclusive scan of the per-chunk allocation counts, then the
+// table that lets k_reserve resolve its free ranks without a tree descent: all
+// allocations of a frame draw from ONE interval of free ranks [T - A, T), which
+// lives in a short run of leaf blocks; win_prefix[j] = free slots before leaf
+// block win_lo + j.
+template <int NT>
+__device__ __forceinline__ void phase_alloc_scan(const FrameArgs &a)
 {
     __shared__ uint32_t scratch[32];
     __shared__ unsigned long long s_carry;
+    __shared__ uint32_t s_blk[2], s_before[2];
     Control *ctl = a.ws.ctl;
-    const int tid = threadIdx.x;
+    const cbtm_pool &p = a.pool;
+    const Geo g = make_geo(p.depth);
+    const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t n = (uint32_t)ctl->n;
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
     if (tid == 0) s_carry = 0;
     __syncthreads();
-    for (uint32_t base = 0; base < nch; base += ADMIT_THREADS) {
+    for (uint32_t base = 0; base < nch; base += NT) {
         const uint32_t c = base + tid;
         const uint32_t v = c < nch ? a.ws.chunk_alloc[c] : 0;
         uint32_t total;
-        const uint32_t incl = block_inclusive_scan<ADMIT_THREADS>(v, scratch, &total);
+        const uint32_t incl = block_inclusive_scan<NT>(v, scratch, &total);
         const unsigned long long carry = s_carry;
         if (c < nch) a.ws.chunk_alloc_off[c] = carry + incl - v;
         __syncthreads();
         if (tid == 0) s_carry = carry + total;
         __syncthreads();
     }
+    const long long A = (long long)s_carry;
+    const long long T = ctl->T;
     if (tid == 0) {
-        const int64_t A = (int64_t)s_carry;
         ctl->A = A;
         ctl->stats[CBTM_STAT_ALLOCATED] = A;
-        a.pool.counter[0] = ctl->T - A; // reservation slack left in the counter (kernels.py:357)
+        p.counter[0] = T - A; // reservation slack left in the counter (kernels.py:357)
+        ctl->win_n = 0;
+    }
+    if (A == 0 || (p.flags & CBTM_POOL_FULL_FREE_CACHE)) return;
+
+    // leaf blocks of the first and the last free rank of the window
+    if (warp < 2) {
+        uint32_t blk, before;
+        warp_find_free_block(p.counters, g, (uint32_t)(warp == 0 ? T - A : T - 1), blk, before);
+        if ((tid & 31) == 0) {
+            s_blk[warp] = blk;
+            s_before[warp] = before;
+        }
+    }
+    __syncthreads();
+    const uint32_t lo = s_blk[0], hi = s_blk[1];
+    const uint32_t nbw = hi - lo + 1;
+    if (nbw > (uint32_t)WIN_MAX) return; // fragmented pool: k_reserve descends per rank
+    if (tid == 0) s_carry = s_before[0];
+    __syncthreads();
+    for (uint32_t base = 0; base < nbw; base += NT) {
+        const uint32_t j = base + tid;
+        const uint32_t z = j < nbw ? g.span - p.counters[g.nblocks + lo + j] : 0;
+        uint32_t total;
+        const uint32_t incl = block_inclusive_scan<NT>(z, scratch, &total);
+        const unsigned long long carry = s_carry;
+        if (j < nbw) a.ws.win_prefix[j] = (uint32_t)(carry + incl - z);
+        __syncthreads();
+        if (tid == 0) s_carry = carry + total;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        a.ws.win_prefix[nbw] = (uint32_t)s_carry;
+        ctl->win_lo = lo;
+        ctl->win_n = nbw;
     }
 }
 
@@ -549,10 +631,16 @@ k_alloc_scan(const __grid_constant__ FrameArgs a)
 // windows are popped from the top of the reserved range exactly like the serial
 // atomic_sub of kernels.py:357-360.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(CHUNK)
-k_reserve(const __grid_constant__ FrameArgs a)
+// The 256 ranks of a chunk draw ONE contiguous interval of free ranks
+// [T - off - total, T - off), total <= 1024.  With the window table the CTA
+// expands the free bits of the few leaf blocks that hold that interval into
+// shared memory (a warp per leaf block, like k_index) and every thread then
+// just picks its slots; without it (fragmented pool) each thread descends.
+__device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t bid, uint32_t nb)
 {
     __shared__ uint32_t scratch[32];
+    __shared__ int32_t slots[4 * CHUNK];
+    __shared__ uint32_t s_j0;
     const cbtm_pool &p = a.pool;
     const Control *ctl = a.ws.ctl;
     const Geo g = make_geo(p.depth);
@@ -560,27 +648,61 @@ k_reserve(const __grid_constant__ FrameArgs a)
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
     const long long T = ctl->T;
     const bool full = p.flags & CBTM_POOL_FULL_FREE_CACHE;
-    const int tid = threadIdx.x;
-    for (uint32_t chunk = blockIdx.x; chunk < nch; chunk += gridDim.x) {
-        if (a.ws.chunk_alloc[chunk] == 0) continue;
+    const uint32_t win_n = ctl->win_n, win_lo = ctl->win_lo;
+    const uint32_t *win = a.ws.win_prefix;
+    const uint32_t *bits32 = reinterpret_cast<const uint32_t *>(p.bits);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
+        const uint32_t total_hint = a.ws.chunk_alloc[chunk];
+        if (total_hint == 0) continue;
         const uint32_t i = chunk * CHUNK + tid;
         const uint32_t na = i < n ? a.ws.nalloc8[i] : 0;
         uint32_t total;
         const uint32_t incl = block_inclusive_scan<CHUNK>(na, scratch, &total);
-        if (!na) continue;
-        const int32_t s = p.cache_live[i];
-        const long long base = T - (long long)(a.ws.chunk_alloc_off[chunk] + incl);
-        for (uint32_t k = 0; k < na; ++k) {
-            const long long r = base + k;
-            int32_t slot;
-            if (full) {
-                slot = p.cache_free[r];
-            } else {
-                slot = cbt_find<false>(p.bits, p.counters, g, (uint32_t)r);
-                p.cache_free[r] = slot;
+        const long long off = (long long)a.ws.chunk_alloc_off[chunk];
+        const long long base = T - (off + incl);
+        const bool coop = !full && win_n != 0;
+        const uint32_t lo_rank = (uint32_t)(T - off - total), hi_rank = (uint32_t)(T - off);
+        if (coop) {
+            // window block holding the lowest rank of the chunk
+            for (uint32_t j = tid; j < win_n; j += CHUNK)
+                if (win[j] <= lo_rank && lo_rank < win[j + 1]) s_j0 = j;
+            __syncthreads();
+            for (uint32_t j = s_j0 + warp; j < win_n; j += CHUNK / 32) {
+                const uint32_t first = win[j]; // free rank of the block's first free slot
+                if (first >= hi_rank) break;
+                const uint32_t b = win_lo + j;
+                const uint32_t valid = g.span >= 1024 ? 32u
+                                     : (lane * 32u >= g.span ? 0u : (g.span - lane * 32u >= 32u ? 32u : g.span - lane * 32u));
+                const uint32_t vmask = valid == 32 ? 0xffffffffu : (valid ? (1u << valid) - 1u : 0u);
+                uint32_t z = valid ? (~bits32[(size_t)b * 32 + lane] & vmask) : 0u;
+                const uint32_t c = __popc(z);
+                uint32_t r = first + warp_inclusive_scan(c) - c; // free rank of this lane's first free slot
+                const int32_t lane_base = (int32_t)(b * g.span + lane * 32);
+                while (z) {
+                    const int k = __ffs(z) - 1;
+                    z &= z - 1;
+                    if (r >= lo_rank && r < hi_rank) slots[r - lo_rank] = lane_base + k;
+                    ++r;
+                }
             }
-            p.reserved[4 * (size_t)s + k] = slot;
+            __syncthreads();
         }
+        if (na) {
+            const int32_t s = p.cache_live[i];
+            for (uint32_t k = 0; k < na; ++k) {
+                const long long r = base + k;
+                int32_t slot;
+                if (full) {
+                    slot = p.cache_free[r];
+                } else {
+                    slot = coop ? slots[(uint32_t)r - lo_rank] : cbt_find<false>(p.bits, p.counters, g, (uint32_t)r);
+                    p.cache_free[r] = slot;
+                }
+                p.reserved[4 * (size_t)s + k] = slot;
+            }
+        }
+        __syncthreads(); // slots / s_j0 are reused by the next chunk
     }
 }
 
@@ -593,7 +715,7 @@ k_reserve(const __grid_constant__ FrameArgs a)
 // *surviving* records, one writer per field (kernels.py:533-594); everything a
 // fill or a redirect reads is either a consumed record (never rewritten), a
 // command word (final since k_scatter), a reservation (final since k_reserve)
-// or the agreement snapshot flags8 (final since k_agree).
+// or the agreement snapshot merge_ref (final since k_agree).
 // ---------------------------------------------------------------------------
 enum { E_TWIN = 0, E_NEXT = 1, E_PREV = 2 };
 enum { H_WHOLE = 0, H_V0 = 1, H_V1 = 2, H_V2 = 3 };
@@ -643,32 +765,65 @@ __device__ __forceinline__ void correspond(int my_side, int my_half, int t_role,
     }
 }
 
+// Everything stage 6/7 ever asks about one pre-update neighbour, fetched with
+// six independent loads (one round trip) instead of a chain of dependent ones.
+struct Neighbour {
+    int32_t slot;     // -1: no neighbour
+    uint32_t cmd;     // its command word (final since k_scatter)
+    int32_t tw, nx, pv;
+    int4 res;         // its reservation (final since k_reserve)
+    int32_t mref;     // its agreed-merge reference (k_agree), -1 if none
+};
+
 struct ApplyCtx {
     const cbtm_pool &p;
-    const uint8_t *flags8;
+    const int32_t *merge_ref;
     uint32_t poison;
 };
 
+__device__ __forceinline__ Neighbour load_neighbour(const ApplyCtx &cx, int32_t slot)
+{
+    Neighbour nbr;
+    nbr.slot = slot;
+    if (slot < 0) {
+        nbr.cmd = 0;
+        nbr.tw = nbr.nx = nbr.pv = nbr.mref = -1;
+        nbr.res = make_int4(-1, -1, -1, -1);
+        return nbr;
+    }
+    const cbtm_pool &p = cx.p;
+    nbr.cmd = p.commands[slot];
+    nbr.tw = p.twins[slot];
+    nbr.nx = p.nexts[slot];
+    nbr.pv = p.prevs[slot];
+    nbr.res = *reinterpret_cast<const int4 *>(p.reserved + 4 * (size_t)slot);
+    nbr.mref = cx.merge_ref[slot];
+    return nbr;
+}
+
+__device__ __forceinline__ int32_t pick4(const int4 &v, int idx)
+{
+    return idx == 0 ? v.x : idx == 1 ? v.y : idx == 2 ? v.z : v.w;
+}
+
 // post-update slot of the record across (my_side, my_half); kernels.py:194-238
-__device__ __forceinline__ int32_t piece_of(ApplyCtx &cx, int32_t target, int my_side, int my_half,
+__device__ __forceinline__ int32_t piece_of(ApplyCtx &cx, const Neighbour &t, int my_side, int my_half,
                                             int32_t backref)
 {
-    if (target < 0) return -1;
-    const cbtm_pool &p = cx.p;
-    const uint32_t cmd = p.commands[target];
-    const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
+    if (t.slot < 0) return -1;
+    const uint32_t sm = t.cmd & CBTM_CMD_SPLIT_MASK;
     if (sm) {
         int role = -1;
         if (my_side == E_TWIN) {
-            if (p.twins[target] == backref) role = E_TWIN;
-            else if (p.nexts[target] == backref) role = E_NEXT;
-            else if (p.prevs[target] == backref) role = E_PREV;
+            if (t.tw == backref) role = E_TWIN;
+            else if (t.nx == backref) role = E_NEXT;
+            else if (t.pv == backref) role = E_PREV;
         } else if (my_side == E_NEXT) {
-            if (p.prevs[target] == backref) role = E_PREV;
-            else if (p.twins[target] == backref) role = E_TWIN;
+            if (t.pv == backref) role = E_PREV;
+            else if (t.tw == backref) role = E_TWIN;
         } else {
-            if (p.nexts[target] == backref) role = E_NEXT;
-            else if (p.twins[target] == backref) role = E_TWIN;
+            if (t.nx == backref) role = E_NEXT;
+            else if (t.tw == backref) role = E_TWIN;
         }
         int idx = -1;
         if (role >= 0) {
@@ -680,29 +835,37 @@ __device__ __forceinline__ int32_t piece_of(ApplyCtx &cx, int32_t target, int my
             ++cx.poison;
             return -2;
         }
-        return p.reserved[4 * (size_t)target + idx];
+        return pick4(t.res, idx);
     }
-    if ((cmd & CBTM_CMD_MERGE) && (cx.flags8[target] & 1)) return merge_parent_slot(p, target);
-    return target;
+    if ((t.cmd & CBTM_CMD_MERGE) && t.mref >= 0) // parent slot held by the merge owner (kernels.py:159-180)
+        return cx.p.reserved[4 * (size_t)(t.mref >> 1) + (t.mref & 1)];
+    return t.slot;
 }
 
-__device__ __forceinline__ bool survives(const ApplyCtx &cx, int32_t x)
+// kernels.py:183-191
+__device__ __forceinline__ bool survives(const Neighbour &t)
 {
-    const uint32_t cmd = cx.p.commands[x];
-    if (cmd & CBTM_CMD_SPLIT_MASK) return false;
-    return !((cmd & CBTM_CMD_MERGE) && (cx.flags8[x] & 1));
+    if (t.cmd & CBTM_CMD_SPLIT_MASK) return false;
+    return !((t.cmd & CBTM_CMD_MERGE) && t.mref >= 0);
 }
 
-// kernels.py:514-530
-__device__ __forceinline__ void redirect_to(const cbtm_pool &p, int32_t target, int32_t old_slot,
+// kernels.py:514-530.  The bundle's pointer values are as good as fresh ones:
+// a field equal to old_slot has exactly one writer (this thread).
+__device__ __forceinline__ void redirect_to(const cbtm_pool &p, const Neighbour &t, int32_t old_slot,
                                             int32_t new_slot, int first)
 {
-    int32_t *primary = first == E_PREV ? p.prevs : p.nexts;
-    if (primary[target] == old_slot) {
-        primary[target] = new_slot;
-        return;
+    if (first == E_PREV) {
+        if (t.pv == old_slot) {
+            p.prevs[t.slot] = new_slot;
+            return;
+        }
+    } else {
+        if (t.nx == old_slot) {
+            p.nexts[t.slot] = new_slot;
+            return;
+        }
     }
-    if (p.twins[target] == old_slot) p.twins[target] = new_slot;
+    if (t.tw == old_slot) p.twins[t.slot] = new_slot;
 }
 
 __device__ __forceinline__ void set_live(uint32_t *bits32, int32_t slot)
@@ -722,76 +885,77 @@ __device__ __forceinline__ void apply_split(ApplyCtx &cx, int32_t s, uint32_t sm
     const uint64_t j = p.ids[s];
     const int32_t nb_n = p.nexts[s], nb_p = p.prevs[s], nb_t = p.twins[s];
     const int4 r4 = *reinterpret_cast<const int4 *>(p.reserved + 4 * (size_t)s);
-    const int32_t r[4] = {r4.x, r4.y, r4.z, r4.w};
-    const int left_n = (sm & CBTM_CMD_SPLIT_P) ? 2 : 1;
-    const int right_n = (sm & CBTM_CMD_SPLIT_N) ? 2 : 1;
-    const int32_t left_last = r[left_n - 1];
-    const int32_t right_first = r[left_n];
+    const Neighbour tn = load_neighbour(cx, nb_n), tp = load_neighbour(cx, nb_p), tt = load_neighbour(cx, nb_t);
+    const bool split_p = sm & CBTM_CMD_SPLIT_P, split_n = sm & CBTM_CMD_SPLIT_N;
+    const int left_n = split_p ? 2 : 1;
+    const int32_t left_last = split_p ? r4.y : r4.x;
+    const int32_t right_first = split_p ? r4.z : r4.y;
+    const int32_t right_second = split_p ? r4.w : r4.z;
 
     // stage 6: fresh records
-    if (left_n == 1) {
-        const int32_t a = r[0];
+    if (!split_p) {
+        const int32_t a = r4.x;
         p.ids[a] = j << 1;
         p.nexts[a] = right_first;
-        p.prevs[a] = piece_of(cx, nb_t, E_TWIN, H_V0, s);
-        p.twins[a] = piece_of(cx, nb_p, E_PREV, H_WHOLE, s);
+        p.prevs[a] = piece_of(cx, tt, E_TWIN, H_V0, s);
+        p.twins[a] = piece_of(cx, tp, E_PREV, H_WHOLE, s);
     } else {
-        const int32_t a = r[0], b = r[1];
+        const int32_t a = r4.x, b = r4.y;
         p.ids[a] = j << 2;
-        p.twins[a] = piece_of(cx, nb_t, E_TWIN, H_V0, s);
+        p.twins[a] = piece_of(cx, tt, E_TWIN, H_V0, s);
         p.nexts[a] = b;
-        p.prevs[a] = piece_of(cx, nb_p, E_PREV, H_V0, s);
+        p.prevs[a] = piece_of(cx, tp, E_PREV, H_V0, s);
         p.ids[b] = (j << 2) + 1;
         p.twins[b] = right_first;
         p.prevs[b] = a;
-        p.nexts[b] = piece_of(cx, nb_p, E_PREV, H_V2, s);
+        p.nexts[b] = piece_of(cx, tp, E_PREV, H_V2, s);
     }
-    if (right_n == 1) {
-        const int32_t c = r[left_n];
+    if (!split_n) {
+        const int32_t c = right_first;
         p.ids[c] = (j << 1) + 1;
         p.prevs[c] = left_last;
-        p.nexts[c] = piece_of(cx, nb_t, E_TWIN, H_V1, s);
-        p.twins[c] = piece_of(cx, nb_n, E_NEXT, H_WHOLE, s);
+        p.nexts[c] = piece_of(cx, tt, E_TWIN, H_V1, s);
+        p.twins[c] = piece_of(cx, tn, E_NEXT, H_WHOLE, s);
     } else {
-        const int32_t c = r[left_n], d = r[left_n + 1];
+        const int32_t c = right_first, d = right_second;
         p.ids[c] = (j << 2) + 2;
         p.twins[c] = left_last;
         p.nexts[c] = d;
-        p.prevs[c] = piece_of(cx, nb_n, E_NEXT, H_V2, s);
+        p.prevs[c] = piece_of(cx, tn, E_NEXT, H_V2, s);
         p.ids[d] = (j << 2) + 3;
         p.prevs[d] = c;
-        p.twins[d] = piece_of(cx, nb_t, E_TWIN, H_V1, s);
-        p.nexts[d] = piece_of(cx, nb_n, E_NEXT, H_V1, s);
+        p.twins[d] = piece_of(cx, tt, E_TWIN, H_V1, s);
+        p.nexts[d] = piece_of(cx, tn, E_NEXT, H_V1, s);
     }
 
     // stage 7: surviving neighbours across unsplit edges (kernels.py:547-561)
-    if (right_n == 1 && nb_n >= 0 && survives(cx, nb_n))
-        redirect_to(p, nb_n, s, r[left_n], E_PREV);
-    if (left_n == 1 && nb_p >= 0 && survives(cx, nb_p))
-        redirect_to(p, nb_p, s, r[0], E_NEXT);
+    if (!split_n && nb_n >= 0 && survives(tn)) redirect_to(p, tn, s, right_first, E_PREV);
+    if (!split_p && nb_p >= 0 && survives(tp)) redirect_to(p, tp, s, r4.x, E_NEXT);
 
     // stage 8
     uint32_t *bits32 = reinterpret_cast<uint32_t *>(p.bits);
     set_free(bits32, s);
-    for (int k = 0; k < left_n + right_n; ++k) set_live(bits32, r[k]);
+    set_live(bits32, r4.x);
+    set_live(bits32, r4.y);
+    if (left_n + (split_n ? 2 : 1) > 2) set_live(bits32, r4.z);
+    if (split_p && split_n) set_live(bits32, r4.w);
 }
 
 // one sibling pair (even id e, odd id o) collapses into parent slot par
-__device__ __forceinline__ void apply_merged_pair(ApplyCtx &cx, int32_t e, int32_t o, int32_t par,
-                                                  int32_t twin_slot)
+__device__ __forceinline__ void apply_merged_pair(ApplyCtx &cx, int32_t e, int32_t o, uint64_t id_e,
+                                                  int32_t par, int32_t twin_slot)
 {
     const cbtm_pool &p = cx.p;
-    const int32_t n_ext = p.twins[o], q_ext = p.twins[e];
-    p.ids[par] = p.ids[e] >> 1;
+    const Neighbour n_ext = load_neighbour(cx, p.twins[o]), q_ext = load_neighbour(cx, p.twins[e]);
+    p.ids[par] = id_e >> 1;
     p.nexts[par] = piece_of(cx, n_ext, E_NEXT, H_WHOLE, o);
     p.prevs[par] = piece_of(cx, q_ext, E_PREV, H_WHOLE, e);
     p.twins[par] = twin_slot;
-    if (n_ext >= 0 && survives(cx, n_ext)) redirect_to(p, n_ext, o, par, E_PREV);
-    if (q_ext >= 0 && survives(cx, q_ext)) redirect_to(p, q_ext, e, par, E_NEXT);
+    if (n_ext.slot >= 0 && survives(n_ext)) redirect_to(p, n_ext, o, par, E_PREV);
+    if (q_ext.slot >= 0 && survives(q_ext)) redirect_to(p, q_ext, e, par, E_NEXT);
 }
 
-__global__ void __launch_bounds__(CHUNK)
-k_apply(const __grid_constant__ FrameArgs a)
+__device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t bid, uint32_t nb)
 {
     __shared__ uint32_t acc[5];
     const cbtm_pool &p = a.pool;
@@ -800,13 +964,22 @@ k_apply(const __grid_constant__ FrameArgs a)
     const int tid = threadIdx.x;
     if (tid < 5) acc[tid] = 0;
     __syncthreads();
-    ApplyCtx cx{p, a.ws.flags8, 0};
+    ApplyCtx cx{p, a.ws.merge_ref, 0};
     uint32_t split_freed = 0, merge_freed = 0, split_alloc = 0, merge_alloc = 0;
     uint32_t *bits32 = reinterpret_cast<uint32_t *>(p.bits);
 
-    for (uint32_t chunk = blockIdx.x; chunk < nch; chunk += gridDim.x) {
+    for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
         const uint32_t i = chunk * CHUNK + tid;
         if (i >= n) continue;
+        if (a.ws.nalloc8[i] == 0) {
+            // not allocating: either untouched, or a non-owner member of an agreed merge
+            const int32_t s = p.cache_live[i];
+            if (a.ws.merge_ref[s] >= 0 && !(p.commands[s] & CBTM_CMD_SPLIT_MASK)) {
+                set_free(bits32, s);
+                ++merge_freed;
+            }
+            continue;
+        }
         const int32_t s = p.cache_live[i];
         const uint32_t cmd = p.commands[s];
         const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
@@ -814,27 +987,28 @@ k_apply(const __grid_constant__ FrameArgs a)
             apply_split(cx, s, sm);
             ++split_freed;
             split_alloc += 2 + ((sm >> 1) & 1) + ((sm >> 2) & 1);
-        } else if ((cmd & CBTM_CMD_MERGE) && (a.ws.flags8[s] & 1)) {
+        } else { // owner of an agreed merge: kernels.py:464-491, 562-594, 624-628
             set_free(bits32, s);
             ++merge_freed;
-            if (cmd & CBTM_CMD_OWNER) { // kernels.py:464-491, 562-594, 624-628
-                const uint64_t js = p.ids[s];
-                const MergeCfg c = merge_config(p, s, js);
-                const bool s_even = !(js & 1);
-                const int32_t p1 = p.reserved[4 * (size_t)s];
-                if (c.kind == 2) {
-                    const int32_t p2 = p.reserved[4 * (size_t)s + 1];
-                    const bool oth_even = !(p.ids[c.oth] & 1);
-                    apply_merged_pair(cx, s_even ? s : c.sib, s_even ? c.sib : s, p1, p2);
-                    apply_merged_pair(cx, oth_even ? c.oth : c.j4, oth_even ? c.j4 : c.oth, p2, p1);
-                    set_live(bits32, p1);
-                    set_live(bits32, p2);
-                    merge_alloc += 2;
-                } else {
-                    apply_merged_pair(cx, s_even ? s : c.sib, s_even ? c.sib : s, p1, -1);
-                    set_live(bits32, p1);
-                    merge_alloc += 1;
-                }
+            const uint64_t js = p.ids[s];
+            const MergeCfg c = merge_config(p, s, js);
+            const bool s_even = !(js & 1);
+            const int32_t p1 = p.reserved[4 * (size_t)s];
+            const uint64_t id_e1 = s_even ? js : p.ids[c.sib];
+            if (c.kind == 2) {
+                const int32_t p2 = p.reserved[4 * (size_t)s + 1];
+                const uint64_t jo = p.ids[c.oth];
+                const bool oth_even = !(jo & 1);
+                const uint64_t id_e2 = oth_even ? jo : p.ids[c.j4];
+                apply_merged_pair(cx, s_even ? s : c.sib, s_even ? c.sib : s, id_e1, p1, p2);
+                apply_merged_pair(cx, oth_even ? c.oth : c.j4, oth_even ? c.j4 : c.oth, id_e2, p2, p1);
+                set_live(bits32, p1);
+                set_live(bits32, p2);
+                merge_alloc += 2;
+            } else {
+                apply_merged_pair(cx, s_even ? s : c.sib, s_even ? c.sib : s, id_e1, p1, -1);
+                set_live(bits32, p1);
+                merge_alloc += 1;
             }
         }
     }
@@ -847,6 +1021,114 @@ k_apply(const __grid_constant__ FrameArgs a)
     if (tid < 5 && acc[tid]) {
         const int slot = tid < 4 ? CBTM_STAT_SPLIT_FREED + tid : CBTM_STAT_POISON;
         atomicAdd((unsigned long long *)&a.ws.ctl->stats[slot], (unsigned long long)acc[tid]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// one kernel per phase (staged path)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(CHUNK)
+k_classify(const __grid_constant__ FrameArgs a, int8_t *verdict_out)
+{
+    phase_classify(a, verdict_out, blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(ADMIT_THREADS) k_admit(const __grid_constant__ FrameArgs a)
+{
+    phase_admit<ADMIT_THREADS>(a);
+}
+
+__global__ void __launch_bounds__(CHUNK) k_scatter(const __grid_constant__ FrameArgs a)
+{
+    phase_scatter(a, blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(CHUNK) k_agree(const __grid_constant__ FrameArgs a)
+{
+    phase_agree(a, blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(ADMIT_THREADS) k_alloc_scan(const __grid_constant__ FrameArgs a)
+{
+    phase_alloc_scan<ADMIT_THREADS>(a);
+}
+
+__global__ void __launch_bounds__(CHUNK) k_reserve(const __grid_constant__ FrameArgs a)
+{
+    phase_reserve(a, blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(CHUNK) k_apply(const __grid_constant__ FrameArgs a)
+{
+    phase_apply(a, blockIdx.x, gridDim.x);
+}
+
+// ---------------------------------------------------------------------------
+// the persistent frame kernel: n_frames full updates in one cooperative launch
+// ---------------------------------------------------------------------------
+constexpr int FRAMES_DYN_SMEM = RED_MAX_STAGES * RED_TILE_BYTES; // 64 KB: index staging (32 KB) / TMA ring
+
+__global__ void __launch_bounds__(CHUNK, 2)
+k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, int do_index)
+{
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(128) uint8_t dyn_smem[];
+    __shared__ __align__(8) uint64_t full[RED_MAX_STAGES];
+    __shared__ uint32_t wroot[2][RED_THREADS / 32];
+    __shared__ bool is_last;
+
+    const cbtm_pool &p = a.pool;
+    const uint32_t bid = blockIdx.x, nb = gridDim.x;
+    const Geo g = make_geo(p.depth);
+    const uint32_t n_tiles = g.nblocks > (uint32_t)RED_TILE_BLOCKS ? g.nblocks / RED_TILE_BLOCKS : 1u;
+    const uint64_t total_bytes = (uint64_t)bitfield_words(p.depth) * 8;
+    const uint32_t per_cta = (n_tiles + nb - 1) / nb;
+    ReduceRing rr{dyn_smem, full, wroot, &is_last,
+                  per_cta < (uint32_t)RED_MAX_STAGES ? (per_cta ? (int)per_cta : 1) : RED_MAX_STAGES, 0};
+    reduce_ring_init(rr);
+    const ReducePublish pub = {a.ws.ctl->stats, p.stats, stats_seq, &a.ws.ctl->seq_frame, a.ws.ctl->phase_t};
+    unsigned long long *stamp = (bid == 0 && threadIdx.x == 0) ? a.ws.ctl->phase_t : nullptr;
+    int32_t *free_list = (p.flags & CBTM_POOL_FULL_FREE_CACHE) ? p.cache_free : nullptr;
+
+    for (int f = 0; f < n_frames; ++f) {
+        if (stamp) stamp[0] = global_ns();
+        if (do_index) {
+            index_phase(reinterpret_cast<const uint32_t *>(p.bits), p.counters, p.depth, p.cache_live,
+                        free_list, p.dispatch, reinterpret_cast<int32_t(*)[1024]>(dyn_smem), bid, nb);
+            grid.sync();
+        }
+        if (stamp) stamp[1] = global_ns();
+        phase_classify(a, nullptr, bid, nb);
+        grid.sync();
+        if (stamp) stamp[2] = global_ns();
+        if (bid == 0) phase_admit<CHUNK>(a);
+        grid.sync();
+        if (stamp) stamp[3] = global_ns();
+        phase_scatter(a, bid, nb);
+        grid.sync();
+        if (stamp) stamp[4] = global_ns();
+        phase_agree(a, bid, nb);
+        grid.sync();
+        if (stamp) stamp[5] = global_ns();
+        if (bid == 0) phase_alloc_scan<CHUNK>(a);
+        grid.sync();
+        if (stamp) stamp[6] = global_ns();
+        phase_reserve(a, bid, nb);
+        grid.sync();
+        if (stamp) stamp[7] = global_ns();
+        phase_apply(a, bid, nb);
+        if (stamp) {
+            __threadfence(); // the publishing CTA reads the stamps after the next barrier
+        }
+        grid.sync();
+        if (stamp) {
+            stamp[8] = global_ns();
+            __threadfence();
+        }
+        reduce_phase(reinterpret_cast<const uint8_t *>(p.bits), p.counters, g.lc, total_bytes, n_tiles,
+                     a.ws.ticket, pub, rr, bid, nb);
+        grid.sync();
     }
 }
 

@@ -48,6 +48,7 @@ class UpdateStats:
     stage_times_us: list = field(default_factory=lambda: [0] * 9)
     reserved_slots: int = 0   # T: slots reserved by admitted commands
     poison: int = 0           # fresh pointers that resolved to the poison -2
+    phase_ns: list = field(default_factory=lambda: [0] * 9)  # device ns per phase (_lib.PHASE_NAMES)
 
     @property
     def structural_ops(self) -> int:
@@ -63,7 +64,17 @@ class UpdateStats:
     @classmethod
     def from_device_words(cls, words, epoch: int, times=None) -> "UpdateStats":
         w = [int(x) for x in words]
-        return cls(epoch=epoch, live_before=w[6], live_after=w[7],
+        if times is None and len(w) >= _lib.STAT_PHASE_NS + 9 and any(w[_lib.STAT_PHASE_NS:_lib.STAT_PHASE_NS + 9]):
+            # device-measured phase times (ns) folded onto the reference's nine stages:
+            # t2 cache pointers = index; t4 generate commands = classify + admit + scatter;
+            # t5 reserve = agree + alloc_scan + reserve; t6 = fused fill/neighbours/bitfield; t9 reduce
+            ph = w[_lib.STAT_PHASE_NS:_lib.STAT_PHASE_NS + 9]
+            us = lambda *ks: sum(ph[k] for k in ks) // 1000  # noqa: E731
+            times = [0, us(0), 0, us(1, 2, 3), us(4, 5, 6), us(7), 0, 0, us(8)]
+            phase_ns = list(ph)
+        else:
+            phase_ns = [0] * 9
+        return cls(phase_ns=phase_ns, epoch=epoch, live_before=w[6], live_after=w[7],
                    splits_applied=w[2], merges_applied=w[3],
                    splits_rejected_oom=w[0], merges_rejected_oom=w[1],
                    split_allocs=w[4], merge_allocs=w[5],
@@ -211,24 +222,27 @@ class ParallelEngine:
         if self.profile:
             events = [t.cuda.Event(enable_timing=True) for _ in range(3)]
             events[0].record()
-        _lib.check(L.cbtm_update_begin(C.byref(pool), stream), "cbtm_update_begin")
-        state._version += 1  # cache_live changed
-        if events:
-            events[1].record()
-
         cv = decide.device_verdict(state) if isinstance(decide, KernelDecide) else None
         keep_alive = None
-        if cv is None:
-            count = int(state.d_counters[1].item())
-            host = self._host_verdicts(state, decide, count)
-            keep_alive = _lib.to_device(host, state.device)
-            cv = _lib.CVerdict()
-            cv.mode = _lib.VERDICT_EXPLICIT
-            cv.explicit_verdicts = _lib.ptr(keep_alive)
-        _lib.check(L.cbtm_update_finish(C.byref(pool), C.byref(cv), stream),
-                   "cbtm_update_finish")
-        if events:
-            events[2].record()
+        if cv is not None and not events:
+            # device verdict source: stages 1-9 in one call (one cooperative launch)
+            _lib.check(L.cbtm_update(C.byref(pool), C.byref(cv), stream), "cbtm_update")
+        else:
+            _lib.check(L.cbtm_update_begin(C.byref(pool), stream), "cbtm_update_begin")
+            state._version += 1  # cache_live changed
+            if events:
+                events[1].record()
+            if cv is None:
+                count = int(state.d_counters[1].item())
+                host = self._host_verdicts(state, decide, count)
+                keep_alive = _lib.to_device(host, state.device)
+                cv = _lib.CVerdict()
+                cv.mode = _lib.VERDICT_EXPLICIT
+                cv.explicit_verdicts = _lib.ptr(keep_alive)
+            _lib.check(L.cbtm_update_finish(C.byref(pool), C.byref(cv), stream),
+                       "cbtm_update_finish")
+            if events:
+                events[2].record()
         state._pinned_stats.copy_(state.d_stats, non_blocking=True)
         state.synchronize()
         del keep_alive

@@ -46,10 +46,12 @@ class TriangulationState:
     ``exact_free_cache=True`` materialises ``cache_free[0:F)`` every frame like
     the reference does (whole-array parity); the default writes only the
     window of free ranks that the frame consumes.
+    ``staged_launches=True`` runs one kernel per pipeline stage instead of the
+    persistent cooperative frame kernel (per-stage profiling).
     """
 
     def __init__(self, mesh, depth: int, device=None,
-                 exact_free_cache: bool = False):
+                 exact_free_cache: bool = False, staged_launches: bool = False):
         H = mesh.n_halfedges
         rank = bisector.root_rank(H)
         if depth < rank:
@@ -63,6 +65,7 @@ class TriangulationState:
         self.max_depth = bisector.max_depth(H)
         self.capacity = cap = 1 << depth
         self.exact_free_cache = bool(exact_free_cache)
+        self.staged_launches = bool(staged_launches)
         self.device = _lib.require_cuda(device)
         L = _lib.load()
         t = _lib.torch()
@@ -112,7 +115,8 @@ class TriangulationState:
             p(self.d_counters), p(self.d_stats), p(self.d_dispatch),
             p(self.d_workspace), self.d_workspace.numel(), self.depth,
             self.rank, int(self.max_depth),
-            _lib.POOL_FULL_FREE_CACHE if self.exact_free_cache else 0)
+            (_lib.POOL_FULL_FREE_CACHE if self.exact_free_cache else 0)
+            | (_lib.POOL_STAGED_LAUNCHES if self.staged_launches else 0))
 
     def _touched(self) -> None:
         """The device arrays changed: drop host snapshots."""
@@ -207,7 +211,8 @@ class TriangulationState:
 
     def clone(self) -> "TriangulationState":
         other = TriangulationState(self.mesh, self.depth, device=self.device,
-                                   exact_free_cache=self.exact_free_cache)
+                                   exact_free_cache=self.exact_free_cache,
+                                   staged_launches=self.staged_launches)
         for k in ("ids", "nexts", "prevs", "twins", "commands", "reserved",
                   "cache_live", "cache_free", "counter", "bits", "counters",
                   "stats"):
@@ -217,11 +222,12 @@ class TriangulationState:
         return other
 
 
-def initialize(mesh, depth: int, device=None,
-               exact_free_cache: bool = False) -> TriangulationState:
+def initialize(mesh, depth: int, device=None, exact_free_cache: bool = False,
+               staged_launches: bool = False) -> TriangulationState:
     """One root bisector per halfedge at slots [0, H) (state.py:139-156)."""
     st = TriangulationState(mesh, depth, device=device,
-                            exact_free_cache=exact_free_cache)
+                            exact_free_cache=exact_free_cache,
+                            staged_launches=staged_launches)
     pool = st.c_pool()
     rc = _lib.load().cbtm_initialize(
         C.byref(pool), _lib.ptr(st.d_he_next), _lib.ptr(st.d_he_prev),

@@ -32,7 +32,7 @@ def _planet_stats(p, frames):
     rows = []
     for cam in cams:
         s, _ = op.update(OracleVerdict.lod(mesh, lod.pack_lod_params(cfg, cam)))
-        rows.append([int(x) for x in s] + [0] * 8)
+        rows.append([int(x) for x in s] + [0] * 24)
     return rows
 
 
@@ -42,7 +42,7 @@ def _worker(rank, world, port, n_planets, frames, queue):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     owned = batch.planets_of_rank(n_planets, world, rank)
-    local = np.array([_planet_stats(p, frames) for p in owned], dtype=np.int64).reshape(len(owned), frames, 16)
+    local = np.array([_planet_stats(p, frames) for p in owned], dtype=np.int64).reshape(len(owned), frames, 32)
     full = batch.gather_stats(local, owned, n_planets, world)
     dist.barrier()
     if rank == 0:
@@ -65,7 +65,7 @@ def test_two_ranks_gather_equals_single_process():
         p.join(timeout=60)
         assert p.exitcode == 0
     single = np.array([_planet_stats(p, frames) for p in range(n_planets)], dtype=np.int64)
-    assert full.shape == (n_planets, frames, 16)
+    assert full.shape == (n_planets, frames, 32)
     assert np.array_equal(full, single)
     # rotated planets really are different workloads
     assert not np.array_equal(single[0], single[1])

@@ -210,7 +210,7 @@ def test_stats_csv_and_convergence():
     assert EpochFactory(lambda e: e * 2)(3) == 6 and EpochFactory.per_epoch
     with pytest.raises(ValueError):
         ParallelEngine(threads=0)
-    words = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 0, 0, 0, 0, 0, 0]
+    words = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10] + [0] * 22
     s = UpdateStats.from_device_words(words, 5)
     assert (s.epoch, s.live_before, s.live_after, s.splits_applied, s.merges_applied,
             s.splits_rejected_oom, s.merges_rejected_oom, s.split_allocs, s.merge_allocs) == \

@@ -18,10 +18,17 @@ from tests.parity import (assert_state_equal, golden_frame_check, load_golden,
 pytestmark = pytest.mark.gpu
 
 
-def run_pair(name, mesh, depth, frames, gpu_decide_of, orc_verdict_of, exact,
+MODES = ["exact", "fast", "fast-staged", "exact-staged"]
+
+
+def run_pair(name, mesh, depth, frames, gpu_decide_of, orc_verdict_of, mode,
              max_depth=None, golden=True, check_every=1):
+    """mode: exact = whole free cache materialised (whole-array parity);
+    fast = only the consumed free-rank window; -staged = one kernel per stage
+    instead of the persistent cooperative frame kernel."""
     from oracle import OraclePool
-    st = initialize(mesh, depth, exact_free_cache=exact)
+    exact = mode.startswith("exact")
+    st = initialize(mesh, depth, exact_free_cache=exact, staged_launches=mode.endswith("staged"))
     op = OraclePool(mesh, depth)
     if max_depth is not None:
         st.max_depth = max_depth
@@ -47,7 +54,7 @@ def run_pair(name, mesh, depth, frames, gpu_decide_of, orc_verdict_of, exact,
     return st, op
 
 
-@pytest.mark.parametrize("exact", [True, False])
+@pytest.mark.parametrize("exact", MODES)
 def test_config1_quad_uniform(exact):
     from oracle import OracleVerdict
     st, _ = run_pair("quad_d16_uniform12", halfedge.single_quad(), 16, 18,
@@ -56,7 +63,7 @@ def test_config1_quad_uniform(exact):
     assert st.count() == 16384
 
 
-@pytest.mark.parametrize("exact", [True, False])
+@pytest.mark.parametrize("exact", MODES)
 def test_const_sources(exact):
     from oracle import OracleVerdict
     run_pair("grid_d9_uniform2", halfedge.quad_grid(2, 2), 9, 3,
@@ -74,7 +81,7 @@ def test_const_sources(exact):
 
 
 @pytest.mark.parametrize("case", tw.SOUP_CASES, ids=lambda c: f"{c[0]}_d{c[1]}")
-@pytest.mark.parametrize("exact", [True, False])
+@pytest.mark.parametrize("exact", MODES)
 def test_random_soups_under_pressure(case, exact):
     """Explicit random verdicts, not budgeted: OOM rejections every frame, so
     the admission tail walk and the top-of-window slot placement are pinned."""
@@ -105,26 +112,35 @@ def _lod_pair(seq):
 def test_config2_cube_sphere_flyin_exact():
     seq = workloads.cube_sphere_flyin(depth=20, frames=64)
     g, o = _lod_pair(seq)
-    run_pair("cube_sphere_flyin_d20", seq.mesh, 20, seq.n_frames, g, o, True)
+    run_pair("cube_sphere_flyin_d20", seq.mesh, 20, seq.n_frames, g, o, "exact")
 
 
-def test_config2_cube_sphere_flyin_fast():
+@pytest.mark.parametrize("mode", ["fast", "fast-staged"])
+def test_config2_cube_sphere_flyin_fast(mode):
     seq = workloads.cube_sphere_flyin(depth=20, frames=64)
     g, o = _lod_pair(seq)
-    run_pair("cube_sphere_flyin_d20", seq.mesh, 20, seq.n_frames, g, o, False, check_every=4)
+    run_pair("cube_sphere_flyin_d20", seq.mesh, 20, seq.n_frames, g, o, mode, check_every=4)
 
 
 def test_config3_stress_earth_sweep_d20():
     """Config 3's camera sweep on a 2^20 pool: 727k OOM rejections."""
     seq = workloads.earth_sweep(depth=20, frames=64)
     g, o = _lod_pair(seq)
-    run_pair("earth_sweep_d20", seq.mesh, 20, seq.n_frames, g, o, True, check_every=4)
+    run_pair("earth_sweep_d20", seq.mesh, 20, seq.n_frames, g, o, "exact", check_every=4)
+
+
+def test_config3_stress_earth_sweep_d20_fast_window():
+    """Same sweep in the default mode: the free-rank window table (and its
+    descent fallback) under heavy reservation pressure."""
+    seq = workloads.earth_sweep(depth=20, frames=64)
+    g, o = _lod_pair(seq)
+    run_pair("earth_sweep_d20", seq.mesh, 20, seq.n_frames, g, o, "fast", check_every=8)
 
 
 def test_config3_short_d22():
     seq = workloads.earth_sweep(depth=22, frames=16)
     g, o = _lod_pair(seq)
-    run_pair("earth_sweep_d22_short", seq.mesh, 22, seq.n_frames, g, o, False, check_every=8)
+    run_pair("earth_sweep_d22_short", seq.mesh, 22, seq.n_frames, g, o, "fast", check_every=8)
 
 
 def test_sequence_runner_matches_per_frame_updates():
@@ -132,12 +148,16 @@ def test_sequence_runner_matches_per_frame_updates():
     seq = workloads.cube_sphere_flyin(depth=18, frames=24)
     a = initialize(seq.mesh, 18)
     b = initialize(seq.mesh, 18)
+    c = initialize(seq.mesh, 18, staged_launches=True)
     with ParallelEngine() as eng:
+        staged = eng.run_lod_sequence(c, seq.params())
         per_frame = [eng.update(a, LodDecide(seq.config, c, seq.mesh), epoch=i)
                      for i, c in enumerate(seq.cameras)]
         batched = eng.run_lod_sequence(b, seq.params())
     assert [stats_words(s) for s in per_frame] == [stats_words(s) for s in batched]
-    ha, hb = a.to_host(), b.to_host()
+    assert [stats_words(s) for s in per_frame] == [stats_words(s) for s in staged]
+    ha, hb, hc = a.to_host(), b.to_host(), c.to_host()
     for k in ha:
         if k != "cache_free":
             assert np.array_equal(ha[k], hb[k]), k
+            assert np.array_equal(ha[k], hc[k]), k
