@@ -200,6 +200,16 @@ int cbtm_classify(const cbtm_pool *pool, const cbtm_verdict *verdict, int8_t *ve
 int cbtm_decode_triangles(const uint64_t *ids, int64_t K, int32_t rank,
                           const double *root_tris, double *out, uintptr_t stream);
 
+/* ---- pointer_violations (state.py:169-203) as a device-side check, so that a
+ *      parity failure can be localised without downloading the pool.  out is
+ *      device i64[CBTM_VALIDATE_WORDS] = {live slots, ids below the root range or
+ *      mapping to an invalid halfedge, ids deeper than max_depth, dangling
+ *      pointers (out of range or to a free slot), pointers without a reciprocal
+ *      pointer (next answered by prev|twin, prev by next|twin, twin by any),
+ *      neighbour depth gaps > 1, first offending slot or -1, 0}. */
+#define CBTM_VALIDATE_WORDS 8
+int cbtm_validate(const cbtm_pool *pool, int32_t n_halfedges, int64_t *out, uintptr_t stream);
+
 /* ---- ParallelEngine.update (pipeline.py:204-322): one nine-stage frame.
  *      cbtm_update            = stages 1-9
  *      cbtm_update_begin      = stages 1-2 (counter reset + cache pointers); after

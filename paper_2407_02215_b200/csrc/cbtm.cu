@@ -311,6 +311,23 @@ int cbtm_decode_triangles(const uint64_t *ids, int64_t K, int32_t rank, const do
     return launch_status();
 }
 
+int cbtm_validate(const cbtm_pool *pool, int32_t n_halfedges, int64_t *out, uintptr_t stream)
+{
+    int rc = check_pool(pool, false);
+    if (rc) return rc;
+    if (!out) return CBTM_E_NULL;
+    if (n_halfedges < 1) return CBTM_E_RANGE;
+    cudaStream_t st = as_stream(stream);
+    // words 0..5 and 7 start at 0, word 6 (first offending slot, taken with atomicMin) at ~0
+    rc = status(cudaMemsetAsync(out, 0, sizeof(int64_t) * CBTM_VALIDATE_WORDS, st));
+    if (rc) return rc;
+    rc = status(cudaMemsetAsync(out + 6, 0xff, sizeof(int64_t), st));
+    if (rc) return rc;
+    k_validate<<<strided_grid((uint64_t)1 << pool->depth, 256, 8), 256, 0, st>>>(
+        *pool, n_halfedges, reinterpret_cast<unsigned long long *>(out));
+    return launch_status();
+}
+
 int cbtm_update_begin(const cbtm_pool *pool, uintptr_t stream)
 {
     const int rc = check_pool(pool, true);

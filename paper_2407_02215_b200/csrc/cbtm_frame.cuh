@@ -56,6 +56,7 @@ struct Workspace {
     uint8_t *need8;   // [N] by live rank: slots to reserve (0 = no command)
     uint8_t *mbits8;  // [N] by live rank: merge command bits of a merge request
     uint8_t *nalloc8; // [N] by live rank: slots actually allocated
+    int32_t *j4s;     // [N] by live rank: fourth member of a valid quad merge configuration
     int32_t *merge_ref; // [N] by slot: -1, or for a member of an agreed merge 2 * owner slot + (1 if the
                         // member sits in the pair opposite to the owner's, i.e. its parent is reserved[owner][1])
     uint32_t *chunk_need;
@@ -89,6 +90,7 @@ inline size_t carve_workspace(void *base, int depth, Workspace *ws)
     w.need8 = (uint8_t *)take(N);
     w.mbits8 = (uint8_t *)take(N);
     w.nalloc8 = (uint8_t *)take(N);
+    w.j4s = (int32_t *)take(4 * N);
     w.merge_ref = (int32_t *)take(4 * N);
     w.chunk_need = (uint32_t *)take(4 * nch);
     w.chunk_need_off = (uint64_t *)take(8 * nch);
@@ -117,30 +119,59 @@ struct FrameArgs {
 struct MergeCfg {
     int kind; // 0 none, 1 boundary pair, 2 quad
     int32_t sib, oth, j4;
+    uint64_t id_sib, id_oth, id_j4; // ids of the members (valid per kind)
 };
 
-__device__ __forceinline__ MergeCfg merge_config(const cbtm_pool &p, int32_t s, uint64_t j1)
+// `nx`, `pv`: the bisector's own next/prev (already loaded by the caller).
+// Loads are grouped so that the whole configuration costs two dependent round
+// trips after nx/pv: {ids[sib], ids[oth], next-or-prev[oth]} then ids[j4].
+__device__ __forceinline__ MergeCfg merge_config(const cbtm_pool &p, uint64_t j1, int32_t nx, int32_t pv)
 {
-    MergeCfg c = {0, -1, -1, -1};
+    MergeCfg c = {0, -1, -1, -1, 0, 0, 0};
     if (depth_of(j1, p.rank) < 1) return c; // roots never merge
     const bool odd = j1 & 1;
-    const int32_t nx = p.nexts[s], pv = p.prevs[s];
     const int32_t sib = odd ? pv : nx;
     const int32_t oth = odd ? nx : pv;
-    if (sib < 0 || (p.ids[sib] >> 1) != (j1 >> 1)) return c;
+    if (sib < 0) return c;
+    const uint64_t js = p.ids[sib];
+    uint64_t jo = 0;
+    int32_t j4 = -1;
+    if (oth >= 0) {
+        jo = p.ids[oth];
+        j4 = odd ? p.nexts[oth] : p.prevs[oth];
+    }
+    if ((js >> 1) != (j1 >> 1)) return c;
+    c.sib = sib;
+    c.id_sib = js;
     if (oth < 0) {
         c.kind = 1;
-        c.sib = sib;
         return c;
     }
-    const uint64_t jo = p.ids[oth];
     if (bit_length64(jo) != bit_length64(j1)) return c;
-    const int32_t j4 = odd ? p.nexts[oth] : p.prevs[oth];
-    if (j4 < 0 || (p.ids[j4] >> 1) != (jo >> 1)) return c;
+    if (j4 < 0) return c;
+    const uint64_t j4id = p.ids[j4];
+    if ((j4id >> 1) != (jo >> 1)) return c;
     c.kind = 2;
-    c.sib = sib;
     c.oth = oth;
     c.j4 = j4;
+    c.id_oth = jo;
+    c.id_j4 = j4id;
+    return c;
+}
+
+// Same configuration for a bisector whose merge request was admitted this
+// frame: k_classify validated it and left the fourth member in j4s (so no
+// pointer chasing here); kind comes from the command word.
+__device__ __forceinline__ MergeCfg merge_config_admitted(uint64_t j1, int32_t nx, int32_t pv, uint32_t cmd,
+                                                          int32_t j4)
+{
+    const bool odd = j1 & 1;
+    MergeCfg c = {1, odd ? pv : nx, -1, -1, 0, 0, 0};
+    if (cmd & CBTM_CMD_QUAD) {
+        c.kind = 2;
+        c.oth = odd ? nx : pv;
+        c.j4 = j4;
+    }
     return c;
 }
 
@@ -162,6 +193,9 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, int8_t *verdi
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+    // per-frame counters start at zero (nothing accumulates before the next barrier)
+    if (!verdict_out && bid == 0 && tid < CBTM_STAT_PHASE_NS && tid != CBTM_STAT_FRAME) a.ws.ctl->stats[tid] = 0;
+
     if (a.vmode == CBTM_VERDICT_LOD) {
         if (tid < CBTM_PRM_WORDS)
             prm[tid] = a.use_prm_seq ? a.ws.prm_seq[(size_t)CBTM_PRM_WORDS * a.ws.ctl->seq_frame + tid]
@@ -175,6 +209,8 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, int8_t *verdi
         if (i < n) {
             const int32_t s = p.cache_live[i];
             const uint64_t id = p.ids[s];
+            // merge requests need these; fetched now so the latency hides behind the classifier
+            const int32_t nx = p.nexts[s], pv = p.prevs[s];
             int v;
             switch (a.vmode) {
             case CBTM_VERDICT_CONST: v = a.vvalue; break;
@@ -190,15 +226,16 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, int8_t *verdi
                     const int d = depth_of(id, p.rank);
                     if (d < p.max_depth) need = 3 * d + 4;
                 } else if (v == 2) {
-                    const MergeCfg c = merge_config(p, s, id);
+                    const MergeCfg c = merge_config(p, id, nx, pv);
                     if (c.kind) {
                         need = 2;
                         mbits = CBTM_CMD_MERGE;
-                        uint64_t lowest = umin64(id, p.ids[c.sib]);
+                        uint64_t lowest = umin64(id, c.id_sib);
                         if (c.kind == 2) {
                             mbits |= CBTM_CMD_QUAD;
-                            lowest = umin64(lowest, p.ids[c.oth]);
-                            lowest = umin64(lowest, p.ids[c.j4]);
+                            lowest = umin64(lowest, c.id_oth);
+                            lowest = umin64(lowest, c.id_j4);
+                            a.ws.j4s[i] = c.j4;
                         }
                         if (lowest == id) mbits |= CBTM_CMD_OWNER;
                     }
@@ -252,7 +289,6 @@ __device__ __forceinline__ void phase_admit(const FrameArgs &a)
     const uint64_t F = ((uint64_t)1 << p.depth) - n;
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
 
-    if (tid < CBTM_STAT_PHASE_NS && tid != CBTM_STAT_FRAME) ctl->stats[tid] = 0;
     if (tid == 0) {
         s_carry = 0;
         s_c0 = nch;
@@ -486,23 +522,25 @@ __device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t bid, ui
                 na = 2 + ((sm >> 1) & 1) + ((sm >> 2) & 1);
             } else if (cmd & CBTM_CMD_MERGE) {
                 const uint64_t js = p.ids[s];
-                const MergeCfg c = merge_config(p, s, js);
-                bool agreed = false;
-                if (c.kind) {
-                    agreed = wants_only_merge(p.commands[c.sib]);
-                    if (agreed && c.kind == 2)
-                        agreed = wants_only_merge(p.commands[c.oth]) && wants_only_merge(p.commands[c.j4]);
+                const MergeCfg c = merge_config_admitted(js, p.nexts[s], p.prevs[s], cmd, a.ws.j4s[i]);
+                // one round trip: the members' command words and ids
+                const uint32_t c_sib = p.commands[c.sib];
+                const uint64_t jb = p.ids[c.sib];
+                uint32_t c_oth = CBTM_CMD_MERGE, c_j4 = CBTM_CMD_MERGE;
+                uint64_t jo = ~0ull, j4 = ~0ull;
+                if (c.kind == 2) {
+                    c_oth = p.commands[c.oth];
+                    c_j4 = p.commands[c.j4];
+                    jo = p.ids[c.oth];
+                    j4 = p.ids[c.j4];
                 }
-                if (agreed) { // owner = member with the smallest id (kernels.py:159-180)
+                if (wants_only_merge(c_sib) && wants_only_merge(c_oth) && wants_only_merge(c_j4)) {
+                    // owner = member with the smallest id (kernels.py:159-180)
                     int32_t owner = s;
                     uint64_t best = js;
-                    const uint64_t jb = p.ids[c.sib];
                     if (jb < best) best = jb, owner = c.sib;
-                    if (c.kind == 2) {
-                        const uint64_t jo = p.ids[c.oth], j4 = p.ids[c.j4];
-                        if (jo < best) best = jo, owner = c.oth;
-                        if (j4 < best) best = j4, owner = c.j4;
-                    }
+                    if (jo < best) best = jo, owner = c.oth;
+                    if (j4 < best) best = j4, owner = c.j4;
                     ref = 2 * owner + ((c.kind == 2 && (js >> 1) != (best >> 1)) ? 1 : 0);
                     if (cmd & CBTM_CMD_OWNER) na = (cmd & CBTM_CMD_QUAD) ? 2 : 1;
                 }
@@ -648,10 +686,17 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t bid, 
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
     const long long T = ctl->T;
     const bool full = p.flags & CBTM_POOL_FULL_FREE_CACHE;
-    const uint32_t win_n = ctl->win_n, win_lo = ctl->win_lo;
     const uint32_t *win = a.ws.win_prefix;
     const uint32_t *bits32 = reinterpret_cast<const uint32_t *>(p.bits);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // one read per CTA, broadcast (the branch on win_n must be CTA-uniform)
+    __shared__ uint32_t s_win[2];
+    if (tid == 0) {
+        s_win[0] = ctl->win_n;
+        s_win[1] = ctl->win_lo;
+    }
+    __syncthreads();
+    const uint32_t win_n = s_win[0], win_lo = s_win[1];
     for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
         const uint32_t total_hint = a.ws.chunk_alloc[chunk];
         if (total_hint == 0) continue;
@@ -991,7 +1036,7 @@ __device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t bid, ui
             set_free(bits32, s);
             ++merge_freed;
             const uint64_t js = p.ids[s];
-            const MergeCfg c = merge_config(p, s, js);
+            const MergeCfg c = merge_config_admitted(js, p.nexts[s], p.prevs[s], cmd, a.ws.j4s[i]);
             const bool s_even = !(js & 1);
             const int32_t p1 = p.reserved[4 * (size_t)s];
             const uint64_t id_e1 = s_even ? js : p.ids[c.sib];
@@ -1130,6 +1175,62 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
                      a.ws.ticket, pub, rr, bid, nb);
         grid.sync();
     }
+}
+
+// ---------------------------------------------------------------------------
+// structural validator (state.py:169-203): one thread per slot, live slots only
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+k_validate(const cbtm_pool p, int n_halfedges, unsigned long long *out)
+{
+    __shared__ unsigned long long acc[6];
+    if (threadIdx.x < 6) acc[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t N = (uint64_t)1 << p.depth;
+    const uint32_t *bits32 = reinterpret_cast<const uint32_t *>(p.bits);
+    auto live = [&](int64_t q) { return (bits32[q >> 5] >> (q & 31)) & 1u; };
+    unsigned cnt[6] = {0, 0, 0, 0, 0, 0};
+    long long first_bad = -1;
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < N;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        if (!live((int64_t)s)) continue;
+        ++cnt[0];
+        const uint64_t id = p.ids[s];
+        bool bad = false;
+        if (id < ((uint64_t)1 << p.rank)) {
+            ++cnt[1];
+            if (first_bad < 0) first_bad = (long long)s;
+            continue;
+        }
+        const int d = depth_of(id, p.rank);
+        const uint64_t he = (id >> d) - ((uint64_t)1 << p.rank);
+        if (he >= (uint64_t)n_halfedges) ++cnt[1], bad = true;
+        if (d > p.max_depth) ++cnt[2], bad = true;
+        const int32_t ptr[3] = {p.nexts[s], p.prevs[s], p.twins[s]};
+#pragma unroll
+        for (int role = 0; role < 3; ++role) { // 0 next, 1 prev, 2 twin
+            const int64_t q = ptr[role];
+            if (q == -1) continue;
+            if (q < 0 || (uint64_t)q >= N || !live(q)) {
+                ++cnt[3], bad = true;
+                continue;
+            }
+            const bool via_next = p.nexts[q] == (int32_t)s, via_prev = p.prevs[q] == (int32_t)s,
+                       via_twin = p.twins[q] == (int32_t)s;
+            const bool answered = role == 0 ? (via_prev || via_twin)
+                                : role == 1 ? (via_next || via_twin)
+                                            : (via_next || via_prev || via_twin);
+            if (!answered) ++cnt[4], bad = true;
+            const int nd = depth_of(p.ids[q], p.rank);
+            if (nd - d > 1 || d - nd > 1) ++cnt[5], bad = true;
+        }
+        if (bad && first_bad < 0) first_bad = (long long)s;
+    }
+    for (int k = 0; k < 6; ++k)
+        if (cnt[k]) atomicAdd(&acc[k], (unsigned long long)cnt[k]);
+    if (first_bad >= 0) atomicMin(reinterpret_cast<unsigned long long *>(out) + 6, (unsigned long long)first_bad);
+    __syncthreads();
+    if (threadIdx.x < 6 && acc[threadIdx.x]) atomicAdd(&out[threadIdx.x], acc[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------------------

@@ -118,7 +118,7 @@ class KernelDecide:
         cv = self.device_verdict(state)
         if cv is None:
             raise NotImplementedError
-        verdicts[start:end] = evaluate_verdicts(state, cv)[start:end]
+        verdicts[start:end] = evaluate_verdicts(state, cv, refresh_index=False)[start:end]
 
 
 class _Const(KernelDecide):
@@ -158,18 +158,23 @@ def lod_verdict(state, prm) -> "_lib.CVerdict":
     cv = _lib.CVerdict()
     cv.mode = _lib.VERDICT_LOD
     cv.root_tris = _lib.ptr(state.d_root_tris)
-    for k in range(_lib.PRM_WORDS):
-        cv.prm[k] = float(prm[k])
+    prm = np.ascontiguousarray(prm, dtype=np.float64)
+    C.memmove(cv.prm, prm.ctypes.data, 8 * _lib.PRM_WORDS)
     return cv
 
 
-def evaluate_verdicts(state: TriangulationState, cv) -> np.ndarray:
-    """int8[count] verdicts of a device verdict source for the CURRENT
-    cache_live order (cbtm_classify; no state is modified)."""
+def evaluate_verdicts(state: TriangulationState, cv, refresh_index: bool = True) -> np.ndarray:
+    """int8[count] verdicts of a device verdict source, in cache_live order
+    (cbtm_classify; records, commands and the CBT are not modified).
+    ``refresh_index`` first rebuilds cache_live from the CBT (stage 2), which
+    is what makes the order well defined outside of an update."""
     t = _lib.torch()
     n = state.count()
     out = t.zeros(max(n, 1), dtype=t.int8, device=state.device)
     pool = state.c_pool()
+    if refresh_index:
+        _lib.check(_lib.load().cbtm_update_begin(C.byref(pool), state.stream()), "cbtm_update_begin")
+        state._version += 1
     rc = _lib.load().cbtm_classify(C.byref(pool), C.byref(cv), _lib.ptr(out),
                                    state.stream())
     _lib.check(rc, "cbtm_classify")

@@ -107,6 +107,17 @@ class TriangulationState:
         return _lib.stream_handle(self.device)
 
     def c_pool(self) -> _lib.CPool:
+        """The cbtm_pool view of this state (cached; max_depth and the mode flags
+        are plain attributes a caller may change between updates)."""
+        key = (int(self.max_depth), self.exact_free_cache, self.staged_launches)
+        cached = getattr(self, "_c_pool", None)
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        pool = self._build_c_pool()
+        self._c_pool = (key, pool)
+        return pool
+
+    def _build_c_pool(self) -> _lib.CPool:
         p = _lib.ptr
         return _lib.CPool(
             p(self.d_ids), p(self.d_nexts), p(self.d_prevs), p(self.d_twins),
@@ -201,6 +212,19 @@ class TriangulationState:
                 _lib.ptr(self.d_root_tris), _lib.ptr(out), self.stream())
             _lib.check(rc, "cbtm_decode_triangles")
         return _lib.to_host(d_ids, np.uint64), _lib.to_host(out)
+
+    def validate_device(self) -> dict:
+        """Counts of structural violations over the live pool, computed on the
+        GPU (cbtm_validate; same checks as :func:`pointer_violations`)."""
+        t = _lib.torch()
+        out = t.empty(8, dtype=t.int64, device=self.device)
+        pool = self.c_pool()
+        rc = _lib.load().cbtm_validate(C.byref(pool), self.mesh.n_halfedges,
+                                       _lib.ptr(out), self.stream())
+        _lib.check(rc, "cbtm_validate")
+        w = [int(x) for x in _lib.to_host(out)]
+        return {"live": w[0], "bad_ids": w[1], "too_deep": w[2], "dangling": w[3],
+                "no_reciprocal": w[4], "depth_gaps": w[5], "first_bad_slot": w[6]}
 
     def memory_bytes(self) -> int:
         names = ("ids", "nexts", "prevs", "twins", "commands", "reserved",

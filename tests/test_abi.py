@@ -43,8 +43,8 @@ def test_size_queries(lib):
     assert lib.cbtm_counter_words(26) == 2 << 16     # heap over 2^16 leaf blocks
     assert lib.cbtm_workspace_bytes(0) == 0 and lib.cbtm_workspace_bytes(31) == 0
     w20, w26 = lib.cbtm_workspace_bytes(20), lib.cbtm_workspace_bytes(26)
-    assert 7 << 20 < w20 < 9 << 20                    # ~7 bytes of scratch per slot
-    assert 7 << 26 < w26 < (7 << 26) + (16 << 20)
+    assert 11 << 20 < w20 < 13 << 20                  # ~11 bytes of scratch per slot
+    assert 11 << 26 < w26 < (11 << 26) + (16 << 20)
 
 
 def test_contract_violations_are_reported_before_launch(lib):
