@@ -327,7 +327,7 @@ def run_gpu(args):
     seq, down, cycle = sweep_params(args.depth, 45.0 * rank)
     K, W = args.steps, args.warmup
     eng = ParallelEngine()
-    state = initialize(seq.mesh, args.depth, device=device)
+    state = initialize(seq.mesh, args.depth, device=device, staged_launches=args.staged)
     eng.run_lod_sequence(state, down)                       # setup: fly to the ground
     eng.run_lod_sequence(state, step_params(cycle, 0, W))   # warm-up steps
     timed_prm = step_params(cycle, W, K)
@@ -420,7 +420,9 @@ def run_gpu(args):
                "sample": f"first {n_cpu} timed frames from the same pool state (stats verified "
                          "equal to the GPU's), oracle port with OpenMP stage 2/classify/stage 9"}
 
-    launches_per_frame = 9  # index, classify, admit, scatter, agree, alloc_scan, reserve, apply, reduce(+publish)
+    # persistent path: ONE cooperative launch (k_frames) runs all K frames, nine phases each;
+    # staged path: index, classify, admit, scatter, agree, alloc_scan, reserve, apply, reduce per frame
+    gpu_launches = 9 * K if args.staged else 1
     line = {
         "metric": METRIC, "value": units_all / (gpu_ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": gpu_ms / K, "higher_is_better": True,
@@ -434,7 +436,7 @@ def run_gpu(args):
         "e2e": {"value": units_all / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms / K,
                 "h2d_bytes_per_step": 8 * _lib.PRM_WORDS, "d2h_bytes_per_step": 8 * _lib.STATS_WORDS,
                 "note": "pool state is device-resident by design; per-frame host input is the camera"},
-        "gpu_launches": launches_per_frame * K,
+        "gpu_launches": gpu_launches, "launch_mode": "staged" if args.staged else "persistent (1 cooperative launch, 9 phases x K frames)",
         "roofline": roofline,
         "config4_d30": config4,
         "cpu_baseline": cpu,
@@ -456,6 +458,9 @@ def main():
     ap.add_argument("--cpu-frames", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-config4", action="store_true")
+    ap.add_argument("--staged", action="store_true",
+                    help="one kernel launch per pipeline stage (for ncu launch lists); default is the "
+                         "persistent cooperative frame kernel")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
