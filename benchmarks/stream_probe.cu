@@ -29,6 +29,11 @@ __global__ void k_touch(const uint4* __restrict__ p, size_t n, unsigned long lon
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) { uint4 a = p[i]; acc += a.x; }
     if (acc == 0x12345678u) atomicAdd(out, 1ull);
 }
+__global__ void k_write(uint4* __restrict__ p, size_t n)
+{
+    const uint4 v = make_uint4(1, 2, 3, 4);
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
 __global__ void k_empty(unsigned long long* out) { if (threadIdx.x == 9999) *out = 1; }
 
 int main()
@@ -55,6 +60,31 @@ int main()
     for (size_t mb : {8, 32, 128, 512, 1024})
         for (int grid : {592, 1184, 2368, 4736})
             run("read", mb << 20, grid, 256);
+    // pure WRITE streams: the ceiling for decode-all (4N bytes written, N/8 read)
+    for (size_t mb : {256, 1024}) {
+        for (int grid : {1184, 4736}) {
+            std::vector<float> ts;
+            for (int r = 0; r < 8; ++r) {
+                k_touch<<<1184, 256>>>(flush, flush_bytes / 16, out);
+                cudaEventRecord(a);
+                k_write<<<grid, 256>>>(buf, (mb << 20) / 16);
+                cudaEventRecord(b); cudaEventSynchronize(b);
+                float ms; cudaEventElapsedTime(&ms, a, b); if (r >= 2) ts.push_back(ms);
+            }
+            std::sort(ts.begin(), ts.end());
+            printf("write      %7.1f MiB grid %5d x  256 : med %8.2f us -> %7.1f GB/s\n", (double)mb, grid, ts[ts.size() / 2] * 1e3, (mb << 20) / (ts[ts.size() / 2] * 1e-3) / 1e9);
+        }
+        std::vector<float> ts;
+        for (int r = 0; r < 8; ++r) {
+            k_touch<<<1184, 256>>>(flush, flush_bytes / 16, out);
+            cudaEventRecord(a);
+            cudaMemsetAsync(buf, 3, mb << 20);
+            cudaEventRecord(b); cudaEventSynchronize(b);
+            float ms; cudaEventElapsedTime(&ms, a, b); if (r >= 2) ts.push_back(ms);
+        }
+        std::sort(ts.begin(), ts.end());
+        printf("memset     %7.1f MiB                   : med %8.2f us -> %7.1f GB/s\n", (double)mb, ts[ts.size() / 2] * 1e3, (mb << 20) / (ts[ts.size() / 2] * 1e-3) / 1e9);
+    }
     run("read512t", 128ull << 20, 1184, 512);
     run("read1024t", 128ull << 20, 592, 1024);
     return 0;

@@ -49,6 +49,7 @@ extern "C" {
 #define CBTM_E_WORKSPACE 3 /* workspace smaller than cbtm_workspace_bytes */
 #define CBTM_E_MODE 4      /* unknown verdict mode / flag */
 #define CBTM_E_RANGE 5     /* count / size argument out of range */
+#define CBTM_E_ALIGN 6     /* bits, reserved, cache_live, cache_free must be 16-byte aligned */
 
 /* command-word bits (state.py:17-25) */
 #define CBTM_CMD_SPLIT_T 1u

@@ -34,7 +34,7 @@ STAT_NAMES = ("oom_splits", "oom_merges", "split_freed", "merge_freed",
 
 _ERRORS = {1: "depth out of range", 2: "required pointer is NULL",
            3: "workspace too small", 4: "unknown verdict mode",
-           5: "argument out of range"}
+           5: "argument out of range", 6: "buffer not 16-byte aligned"}
 
 
 class CbtmError(RuntimeError):

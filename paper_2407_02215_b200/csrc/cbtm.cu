@@ -82,6 +82,9 @@ int check_pool(const cbtm_pool *p, bool need_ws)
         if (p->workspace_bytes < carve_workspace(nullptr, p->depth, nullptr)) return CBTM_E_WORKSPACE;
     }
     if (p->rank < 1 || p->rank > 62 || p->max_depth < 0) return CBTM_E_RANGE;
+    // 128-bit accesses: reserved rows, index lists, bitfield lines
+    if (((uintptr_t)p->reserved | (uintptr_t)p->cache_live | (uintptr_t)p->cache_free | (uintptr_t)p->bits) & 15)
+        return CBTM_E_ALIGN;
     return 0;
 }
 
@@ -200,6 +203,7 @@ int cbtm_sum_reduce(const uint64_t *bits, uint32_t *counters, int depth, void *w
 {
     if (bad_depth(depth)) return CBTM_E_DEPTH;
     if (!bits || !counters || !workspace) return CBTM_E_NULL;
+    if ((uintptr_t)bits & 15) return CBTM_E_ALIGN; // TMA bulk copies
     if (workspace_bytes < 256) return CBTM_E_WORKSPACE;
     // the ticket is word 0 of the workspace (also of a pool's frame workspace); it
     // must be zero on entry and the last CTA leaves it zero again
@@ -236,6 +240,7 @@ int cbtm_index(const uint64_t *bits, const uint32_t *counters, int depth, int32_
 {
     if (bad_depth(depth)) return CBTM_E_DEPTH;
     if (!bits || !counters || !cache_live) return CBTM_E_NULL;
+    if (((uintptr_t)bits | (uintptr_t)cache_live | (uintptr_t)cache_free) & 15) return CBTM_E_ALIGN;
     const Geo g = make_geo(depth);
     k_index<<<strided_grid(g.nblocks, IDX_WARPS, 6), IDX_WARPS * 32, 0, as_stream(stream)>>>(
         reinterpret_cast<const uint32_t *>(bits), counters, depth, cache_live, cache_free, dispatch);

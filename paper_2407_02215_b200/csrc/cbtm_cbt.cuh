@@ -338,30 +338,77 @@ k_decode(const uint64_t *__restrict__ bits, const uint32_t *__restrict__ counter
 // Indexation (pipeline stage 2, k_cache_pointers kernels.py:244-252) as a
 // stream compaction.  One warp per 1024-slot leaf block:
 //   * its rank offset comes from the counter heap (sum of the left siblings on
-//     the root path -- all addresses known up front, one load per lane),
-//   * the block's slots are expanded into a 4 KB shared staging area (set bits
-//     from the front, unset bits behind them) and copied out coalesced.
-// Blocks with no set bit are skipped without touching the bitfield when the
-// free list is not requested.
+//     the root path -- all addresses known up front, one load per lane);
+//   * lane l owns word l of the block; the warp walks the 32 words, each
+//     broadcast with one shuffle, and lane l handles BIT l of the current word:
+//     its rank inside the word is a popcount under a lane mask, the running
+//     rank is warp-uniform arithmetic -- no data-dependent loops, ~12
+//     instructions per 32 slots.  Slots go to a shared staging area (set bits
+//     first, unset bits behind them), each list placed so that its staging
+//     index is congruent to its global index modulo 32;
+//   * the copy-out therefore moves 128-byte-aligned lines with 128-bit shared
+//     loads and 128-bit global stores (scalar stores only on the two edge
+//     vectors of a list).
+// ncu on the first versions showed this kernel bound by instruction issue
+// (71-77 % issue slots busy at ~3.3 TB/s), not by HBM (a bare write stream
+// reaches 6-7 TB/s here), hence the instruction diet.
+// Blocks with no set bit are skipped from their counter without touching the
+// bitfield when the free list is not requested; so are empty words.
+// Plain (coherent) loads only: inside the persistent frame kernel the bitfield
+// and the counters were written earlier in the same launch.
 // ---------------------------------------------------------------------------
 constexpr int IDX_WARPS = 8;
+constexpr int IDX_STAGE_WORDS = 1152; // 1024 slots + alignment slack of both lists
 
-// staging index swizzle: element i lives at i ^ ((i >> 5) & 31).  Expansion
-// writes from different lanes are typically ~32 apart (same bank unswizzled);
-// the copy-out reads 32 consecutive elements, which stay conflict free.
-__device__ __forceinline__ uint32_t stage_at(uint32_t i) { return i ^ ((i >> 5) & 31u); }
+// out[gbase + off .. gbase + off + count) = st[off .. off + count); gbase is a multiple of 32
+// entries (128 bytes) and st is 16-byte aligned, so interior vectors move as int4.
+__device__ __forceinline__ void copy_out_lines(int32_t *out, uint32_t gbase, uint32_t off, uint32_t count,
+                                               const int32_t *st, int lane)
+{
+    const uint32_t total = off + count;
+    for (uint32_t e0 = 4u * lane; e0 < total; e0 += 128u) {
+        if (e0 + 4u <= off) continue;
+        const int4 x = *reinterpret_cast<const int4 *>(st + e0);
+        if (e0 >= off && e0 + 4u <= total) {
+            *reinterpret_cast<int4 *>(out + gbase + e0) = x;
+        } else {
+            if (e0 >= off && e0 < total) out[gbase + e0] = x.x;
+            if (e0 + 1 >= off && e0 + 1 < total) out[gbase + e0 + 1] = x.y;
+            if (e0 + 2 >= off && e0 + 2 < total) out[gbase + e0 + 2] = x.z;
+            if (e0 + 3 >= off && e0 + 3 < total) out[gbase + e0 + 3] = x.w;
+        }
+    }
+}
 
-// `stage` is IDX_WARPS x 1024 words of shared memory.  Plain (coherent) loads
-// only: inside the persistent frame kernel the bitfield and the counters were
-// written earlier in the same launch.
+// out[first .. first + count) = slot0, slot0 + 1, ... (a block that is entirely live or free)
+__device__ __forceinline__ void fill_run_lines(int32_t *out, uint32_t first, uint32_t count, int32_t slot0,
+                                               int lane)
+{
+    const uint32_t off = first & 31u, gbase = first - off, total = off + count;
+    for (uint32_t e0 = 4u * lane; e0 < total; e0 += 128u) {
+        if (e0 + 4u <= off) continue;
+        const int32_t v = slot0 + (int32_t)e0 - (int32_t)off;
+        if (e0 >= off && e0 + 4u <= total) {
+            *reinterpret_cast<int4 *>(out + gbase + e0) = make_int4(v, v + 1, v + 2, v + 3);
+        } else {
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k)
+                if (e0 + k >= off && e0 + k < total) out[gbase + e0 + k] = v + (int32_t)k;
+        }
+    }
+}
+
 __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32_t *counters, int depth,
                                             int32_t *cache_live, int32_t *cache_free, uint32_t *dispatch,
-                                            int32_t (*stage)[1024], uint32_t bid, uint32_t nb)
+                                            int32_t (*stage)[IDX_STAGE_WORDS], uint32_t bid, uint32_t nb)
 {
     const Geo g = make_geo(depth);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t gwarp = bid * IDX_WARPS + warp;
     const uint32_t nwarps = nb * IDX_WARPS;
+    const uint32_t lane_lt = (1u << lane) - 1u;
+    const bool want_free = cache_free != nullptr;
+    int32_t *st = stage[warp];
 
     if (dispatch && bid == 0 && threadIdx.x == 0) {
         const uint32_t n = counters[1];
@@ -371,14 +418,13 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
         dispatch[3] = n;
     }
 
-    int32_t *st = stage[warp];
     // this warp owns leaf blocks gwarp + k * nwarps; lane k fetches the count of the
     // k-th of them, so one round trip tells the warp which of its next 32 blocks
     // hold anything (a sparse pool skips almost all of them)
     for (uint32_t k0 = 0; gwarp + (uint64_t)k0 * nwarps < g.nblocks; k0 += 32) {
         const uint64_t mine = gwarp + (uint64_t)(k0 + lane) * nwarps;
         const uint32_t my_cnt = mine < g.nblocks ? counters[g.nblocks + mine] : 0u;
-        unsigned todo = __ballot_sync(FULL_MASK, mine < g.nblocks && (my_cnt != 0 || cache_free != nullptr));
+        unsigned todo = __ballot_sync(FULL_MASK, mine < g.nblocks && (my_cnt != 0 || want_free));
         while (todo) {
             const int src = __ffs(todo) - 1;
             todo &= todo - 1;
@@ -394,45 +440,59 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
             const uint32_t ones_before = warp_sum(part);
             const uint32_t zeros_before = b * g.span - ones_before;
             const int32_t base = (int32_t)(b * g.span);
+
+            if (cnt == 0 || cnt == g.span) { // uniform block: no expansion needed
+                fill_run_lines(cnt ? cache_live : cache_free, cnt ? ones_before : zeros_before, g.span, base, lane);
+                continue;
+            }
+
+            // staging: ones at [o1, o1 + cnt), zeros at [z0, z0 + zcnt); both congruent to their
+            // global index modulo 32
             const uint32_t zcnt = g.span - cnt;
-
-            if (cnt == 0) { // all free
-                for (uint32_t i = lane; i < g.span; i += 32) cache_free[zeros_before + i] = base + (int32_t)i;
-                continue;
-            }
-            if (cnt == g.span) { // all live
-                for (uint32_t i = lane; i < g.span; i += 32) cache_live[ones_before + i] = base + (int32_t)i;
-                continue;
-            }
-
-            const uint32_t valid = g.span >= 1024 ? 32u
-                                 : (lane * 32u >= g.span ? 0u : (g.span - lane * 32u >= 32u ? 32u : g.span - lane * 32u));
-            uint32_t w = valid ? bits32[(size_t)b * 32 + lane] : 0u;
-            const uint32_t vmask = valid == 32 ? 0xffffffffu : ((1u << valid) - 1u);
-            w &= vmask;
-            const uint32_t c = __popc(w);
-            const uint32_t incl = warp_inclusive_scan(c);
-            uint32_t o1 = incl - c;                     // set bits before this lane
-            uint32_t o0 = cnt + (lane * 32u > g.span ? g.span : lane * 32u) - o1; // staged after the ones
-            const int32_t lane_base = base + lane * 32;
-            uint32_t ones = w;
-            while (ones) {
-                const int k = __ffs(ones) - 1;
-                ones &= ones - 1;
-                st[stage_at(o1++)] = lane_base + k;
-            }
-            if (cache_free) {
-                uint32_t zeros = ~w & vmask;
-                while (zeros) {
-                    const int k = __ffs(zeros) - 1;
-                    zeros &= zeros - 1;
-                    st[stage_at(o0++)] = lane_base + k;
+            const uint32_t o1 = ones_before & 31u;
+            const uint32_t zline = (o1 + cnt + 31u) & ~31u;
+            const uint32_t z0 = zline + (zeros_before & 31u);
+            uint32_t p1 = o1, p0 = z0;
+            if (g.span == 1024u) { // every word fully valid (all pools with D >= 10)
+                const uint32_t own = bits32[(size_t)b * 32 + lane];
+#pragma unroll 8
+                for (int w = 0; w < 32; ++w) {
+                    const uint32_t word = __shfl_sync(FULL_MASK, own, w);
+                    if (word == 0u && !want_free) continue;
+                    const uint32_t r1 = __popc(word & lane_lt);
+                    const int32_t slot = base + w * 32 + lane;
+                    if ((word >> lane) & 1u)
+                        st[p1 + r1] = slot;
+                    else if (want_free)
+                        st[p0 + (uint32_t)lane - r1] = slot;
+                    const uint32_t c = __popc(word);
+                    p1 += c;
+                    p0 += 32u - c;
+                }
+            } else { // tiny pool: a single partial block
+                const uint32_t nwords = (g.span + 31u) / 32u;
+                const uint32_t own = (uint32_t)lane < nwords ? bits32[(size_t)b * 32 + lane] : 0u;
+                for (uint32_t w = 0; w < nwords; ++w) {
+                    const uint32_t valid = g.span - w * 32u >= 32u ? 32u : g.span - w * 32u;
+                    const uint32_t vmask = valid == 32u ? 0xffffffffu : (1u << valid) - 1u;
+                    const uint32_t word = __shfl_sync(FULL_MASK, own, (int)w) & vmask;
+                    const uint32_t r1 = __popc(word & lane_lt);
+                    const int32_t slot = base + (int32_t)(w * 32u) + lane;
+                    if ((uint32_t)lane < valid) {
+                        if ((word >> lane) & 1u)
+                            st[p1 + r1] = slot;
+                        else if (want_free)
+                            st[p0 + (uint32_t)lane - r1] = slot;
+                    }
+                    const uint32_t c = __popc(word);
+                    p1 += c;
+                    p0 += valid - c;
                 }
             }
             __syncwarp();
-            for (uint32_t i = lane; i < cnt; i += 32) cache_live[ones_before + i] = st[stage_at(i)];
-            if (cache_free)
-                for (uint32_t i = lane; i < zcnt; i += 32) cache_free[zeros_before + i] = st[stage_at(cnt + i)];
+            copy_out_lines(cache_live, ones_before - o1, o1, cnt, st, lane);
+            if (want_free) copy_out_lines(cache_free, zeros_before - (zeros_before & 31u), zeros_before & 31u, zcnt,
+                                          st + zline, lane);
             __syncwarp();
         }
     }
@@ -442,7 +502,7 @@ __global__ void __launch_bounds__(IDX_WARPS * 32)
 k_index(const uint32_t *bits32, const uint32_t *counters, int depth, int32_t *cache_live,
         int32_t *cache_free, uint32_t *dispatch)
 {
-    __shared__ int32_t stage[IDX_WARPS][1024];
+    __shared__ __align__(16) int32_t stage[IDX_WARPS][IDX_STAGE_WORDS];
     index_phase(bits32, counters, depth, cache_live, cache_free, dispatch, stage, blockIdx.x, gridDim.x);
 }
 

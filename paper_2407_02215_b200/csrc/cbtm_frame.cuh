@@ -1111,7 +1111,7 @@ __global__ void __launch_bounds__(CHUNK) k_apply(const __grid_constant__ FrameAr
 // ---------------------------------------------------------------------------
 // the persistent frame kernel: n_frames full updates in one cooperative launch
 // ---------------------------------------------------------------------------
-constexpr int FRAMES_DYN_SMEM = RED_MAX_STAGES * RED_TILE_BYTES; // 64 KB: index staging (32 KB) / TMA ring
+constexpr int FRAMES_DYN_SMEM = RED_MAX_STAGES * RED_TILE_BYTES; // 64 KB: index staging (36 KB) / TMA ring / upper-tree heap
 
 __global__ void __launch_bounds__(CHUNK, 2)
 k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, int do_index)
@@ -1140,7 +1140,7 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         if (stamp) stamp[0] = global_ns();
         if (do_index) {
             index_phase(reinterpret_cast<const uint32_t *>(p.bits), p.counters, p.depth, p.cache_live,
-                        free_list, p.dispatch, reinterpret_cast<int32_t(*)[1024]>(dyn_smem), bid, nb);
+                        free_list, p.dispatch, reinterpret_cast<int32_t(*)[IDX_STAGE_WORDS]>(dyn_smem), bid, nb);
             grid.sync();
         }
         if (stamp) stamp[1] = global_ns();
