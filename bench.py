@@ -420,8 +420,8 @@ def run_gpu(args):
                "sample": f"first {n_cpu} timed frames from the same pool state (stats verified "
                          "equal to the GPU's), oracle port with OpenMP stage 2/classify/stage 9"}
 
-    # persistent path: ONE cooperative launch (k_frames) runs all K frames, nine phases each;
-    # staged path: index, classify, admit, scatter, agree, alloc_scan, reserve, apply, reduce per frame
+    # persistent path: ONE cooperative launch (k_frames) runs all K frames, six phases each;
+    # staged path: index, classify, admit, scatter, agree, reserve, apply, upper_reduce, publish per frame
     gpu_launches = 9 * K if args.staged else 1
     line = {
         "metric": METRIC, "value": units_all / (gpu_ms * 1e-3), "unit": UNIT, "n_gpus": world,
@@ -436,7 +436,7 @@ def run_gpu(args):
         "e2e": {"value": units_all / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms / K,
                 "h2d_bytes_per_step": 8 * _lib.PRM_WORDS, "d2h_bytes_per_step": 8 * _lib.STATS_WORDS,
                 "note": "pool state is device-resident by design; per-frame host input is the camera"},
-        "gpu_launches": gpu_launches, "launch_mode": "staged" if args.staged else "persistent (1 cooperative launch, 9 phases x K frames)",
+        "gpu_launches": gpu_launches, "launch_mode": "staged" if args.staged else "persistent (1 cooperative launch, 6 phases x K frames)",
         "roofline": roofline,
         "config4_d30": config4,
         "cpu_baseline": cpu,

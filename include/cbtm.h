@@ -84,11 +84,13 @@ enum {
     CBTM_STAT_ALLOCATED = 9, /* A: slots actually allocated              */
     CBTM_STAT_POISON = 10,   /* fresh pointers resolved to the poison -2 */
     CBTM_STAT_FRAME = 11,    /* frames applied to this pool so far       */
-    /* words 16..24: device time of each phase of the frame in ns (persistent
-     * frame kernel only; 0 on the staged path): index, classify, admit, scatter,
-     * agree, alloc_scan, reserve, apply, sum_reduce -- cf. UpdateStats.stage_times_us */
+    /* words 16..21: device time of each phase of the frame in ns (persistent
+     * frame kernel only; 0 on the staged path): index (stages 1-3), classify +
+     * admission + command scatter (stage 4), merge agreement (stage 5a), slot
+     * hand-out (stage 5b), apply (stages 6-8), sum reduction + stats publish
+     * (stage 9) -- cf. UpdateStats.stage_times_us */
     CBTM_STAT_PHASE_NS = 16,
-    CBTM_STAT_PHASES = 9
+    CBTM_STAT_PHASES = 6
 };
 
 /* One bisector pool == the reference's TriangulationState (state.py:32-55).

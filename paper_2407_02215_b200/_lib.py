@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libcbtm.so")
 PRM_WORDS = 23
 STATS_WORDS = 32
 STAT_PHASE_NS = 16
-PHASE_NAMES = ("index", "classify", "admit", "scatter", "agree", "alloc_scan", "reserve", "apply", "sum_reduce")
+PHASE_NAMES = ("index", "classify_admit_scatter", "agree", "reserve", "apply", "reduce_publish")
 MIN_DEPTH = 1
 MAX_DEPTH_ABI = 30
 

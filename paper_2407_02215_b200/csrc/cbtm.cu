@@ -116,37 +116,61 @@ int fill_args(const cbtm_pool *pool, const cbtm_verdict *v, FrameArgs *a)
     return 0;
 }
 
+// Co-resident grid for a kernel of CHUNK threads: the look-back scans of the frame
+// phases wait on other CTAs, so no CTA may be left waiting for an SM.
+template <typename K>
+unsigned resident_grid(K kernel, int depth, int cap_per_sm, size_t dyn_smem)
+{
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, CHUNK, dyn_smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    if (per_sm > cap_per_sm) per_sm = cap_per_sm;
+    const uint64_t want = (((uint64_t)1 << depth) + CHUNK - 1) / CHUNK; // tiny pools: fewer CTAs
+    const uint64_t cap = (uint64_t)sm_count() * per_sm;
+    return (unsigned)(want < cap ? want : cap);
+}
+
 unsigned frame_grid(int depth)
 {
     return strided_grid((uint64_t)1 << depth, CHUNK, 8);
 }
 
-int index_launch(const cbtm_pool *pool, cudaStream_t st)
+int index_launch(const cbtm_pool *pool, bool reset_commands, cudaStream_t st)
 {
     const Geo g = make_geo(pool->depth);
     int32_t *freep = (pool->flags & CBTM_POOL_FULL_FREE_CACHE) ? pool->cache_free : nullptr;
     const unsigned grid = strided_grid(g.nblocks, IDX_WARPS, 6);
     k_index<<<grid, IDX_WARPS * 32, 0, st>>>(reinterpret_cast<const uint32_t *>(pool->bits),
                                              pool->counters, pool->depth, pool->cache_live, freep,
-                                             pool->dispatch);
+                                             pool->dispatch, reset_commands ? pool->commands : nullptr);
     return launch_status();
 }
 
-// stages 3-9, one kernel per phase (staged path)
-int finish_staged(const FrameArgs &a, int64_t *stats_seq, cudaStream_t st)
+int upper_reduce_launch(const FrameArgs &a, int64_t *stats_seq, cudaStream_t st)
 {
-    const unsigned grid = frame_grid(a.pool.depth);
-    k_classify<<<grid, CHUNK, 0, st>>>(a, nullptr);
-    k_admit<<<1, ADMIT_THREADS, 0, st>>>(a);
-    k_scatter<<<grid, CHUNK, 0, st>>>(a);
-    k_agree<<<grid, CHUNK, 0, st>>>(a);
-    k_alloc_scan<<<1, ADMIT_THREADS, 0, st>>>(a);
-    k_reserve<<<grid, CHUNK, 0, st>>>(a);
-    k_apply<<<grid, CHUNK, 0, st>>>(a);
+    const Geo g = make_geo(a.pool.depth);
+    const unsigned tiles = g.nblocks > (unsigned)UP_TILE ? g.nblocks / UP_TILE : 1u;
+    const unsigned cap = (unsigned)sm_count() * 2;
+    k_upper_reduce<<<tiles < cap ? tiles : cap, RED_THREADS, 0, st>>>(a.pool.bits, a.ws.dirty, a.pool.counters, g.lc);
+    k_publish<<<1, CHUNK, 0, st>>>(a, stats_seq);
+    return launch_status();
+}
+
+// stages 3-9, one kernel per phase (staged path).  with_reset: stage 3 was not
+// folded into the index kernel (cbtm_update_finish).
+int finish_staged(const FrameArgs &a, int64_t *stats_seq, bool with_reset, cudaStream_t st)
+{
+    const int d = a.pool.depth;
+    if (with_reset) k_reset<<<frame_grid(d), CHUNK, 0, st>>>(a);
+    k_classify_frame<<<resident_grid(k_classify_frame, d, 2, 0), CHUNK, 0, st>>>(a);
+    k_admit<<<1, CHUNK, 0, st>>>(a);
+    k_scatter<<<frame_grid(d), CHUNK, 0, st>>>(a);
+    k_agree<<<frame_grid(d), CHUNK, 0, st>>>(a);
+    k_reserve<<<frame_grid(d), CHUNK, 0, st>>>(a);
+    k_apply<<<frame_grid(d), CHUNK, 0, st>>>(a);
     const int rc = launch_status();
     if (rc) return rc;
-    const ReducePublish pub = {a.ws.ctl->stats, a.pool.stats, stats_seq, &a.ws.ctl->seq_frame, nullptr};
-    return reduce_launch(a.pool.bits, a.pool.counters, a.pool.depth, a.ws.ticket, pub, st);
+    return upper_reduce_launch(a, stats_seq, st);
 }
 
 // Co-resident grid of the persistent frame kernel (0: cooperative launch unavailable)
@@ -243,7 +267,7 @@ int cbtm_index(const uint64_t *bits, const uint32_t *counters, int depth, int32_
     if (((uintptr_t)bits | (uintptr_t)cache_live | (uintptr_t)cache_free) & 15) return CBTM_E_ALIGN;
     const Geo g = make_geo(depth);
     k_index<<<strided_grid(g.nblocks, IDX_WARPS, 6), IDX_WARPS * 32, 0, as_stream(stream)>>>(
-        reinterpret_cast<const uint32_t *>(bits), counters, depth, cache_live, cache_free, dispatch);
+        reinterpret_cast<const uint32_t *>(bits), counters, depth, cache_live, cache_free, dispatch, nullptr);
     return launch_status();
 }
 
@@ -277,7 +301,7 @@ int cbtm_initialize(const cbtm_pool *pool, const int32_t *he_next, const int32_t
     carve_workspace(pool->workspace, pool->depth, &ws);
     cudaStream_t st = as_stream(stream);
     k_initialize<<<strided_grid((uint64_t)1 << pool->depth, 256, 8), 256, 0, st>>>(
-        *pool, he_next, he_prev, he_twin, n_halfedges, ws.ctl, ws.ticket);
+        *pool, he_next, he_prev, he_twin, n_halfedges, ws);
     rc = launch_status();
     if (rc) return rc;
     return reduce_launch(pool->bits, pool->counters, pool->depth, ws.ticket, kNoPublish, st);
@@ -337,7 +361,7 @@ int cbtm_update_begin(const cbtm_pool *pool, uintptr_t stream)
 {
     const int rc = check_pool(pool, true);
     if (rc) return rc;
-    return index_launch(pool, as_stream(stream));
+    return index_launch(pool, false, as_stream(stream));
 }
 
 int cbtm_update_finish(const cbtm_pool *pool, const cbtm_verdict *verdict, uintptr_t stream)
@@ -349,7 +373,7 @@ int cbtm_update_finish(const cbtm_pool *pool, const cbtm_verdict *verdict, uintp
     rc = fill_args(pool, verdict, &a);
     if (rc) return rc;
     const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth);
-    if (!grid) return finish_staged(a, nullptr, as_stream(stream));
+    if (!grid) return finish_staged(a, nullptr, true, as_stream(stream));
     return frames_launch(a, 1, nullptr, 0, grid, as_stream(stream));
 }
 
@@ -363,8 +387,8 @@ int cbtm_update(const cbtm_pool *pool, const cbtm_verdict *verdict, uintptr_t st
     if (rc) return rc;
     const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth);
     if (!grid) {
-        rc = index_launch(pool, as_stream(stream));
-        return rc ? rc : finish_staged(a, nullptr, as_stream(stream));
+        rc = index_launch(pool, true, as_stream(stream));
+        return rc ? rc : finish_staged(a, nullptr, false, as_stream(stream));
     }
     return frames_launch(a, 1, nullptr, 1, grid, as_stream(stream));
 }
@@ -401,9 +425,9 @@ int cbtm_run_lod_sequence(const cbtm_pool *pool, const double *root_tris, const 
             if (rc) return rc;
         } else {
             for (int32_t f = 0; f < batch; ++f) {
-                rc = index_launch(pool, st);
+                rc = index_launch(pool, true, st);
                 if (rc) return rc;
-                rc = finish_staged(a, so, st);
+                rc = finish_staged(a, so, false, st);
                 if (rc) return rc;
             }
         }

@@ -30,13 +30,13 @@ constexpr int RED_TILE_BYTES = 16384;
 constexpr int RED_TILE_BLOCKS = 128; // leaf blocks per tile
 constexpr int RED_MAX_STAGES = 4;
 
-// end-of-frame bookkeeping folded into the last CTA (all NULL when standalone)
+// end-of-frame bookkeeping (publish_frame)
 struct ReducePublish {
     int64_t *ctl_stats;  // Control::stats
     int64_t *pool_stats; // cbtm_pool::stats
     int64_t *stats_seq;  // per-frame rows of a sequence run
     uint32_t *seq_frame; // Control::seq_frame
-    const unsigned long long *phase_t; // Control::phase_t (persistent kernel) or NULL
+    const unsigned long long *phase_t; // this frame's Control::phase_t row (persistent kernel) or NULL
 };
 
 __device__ __forceinline__ unsigned long long global_ns()
@@ -67,6 +67,8 @@ __device__ __forceinline__ void publish_frame(const ReducePublish &pub, uint32_t
         }
         if (pub.pool_stats) pub.pool_stats[tid] = v;
         if (pub.stats_seq) pub.stats_seq[(size_t)CBTM_STATS_WORDS * (*pub.seq_frame) + tid] = v;
+        // the per-frame counters start the next frame at zero
+        if (tid < CBTM_STAT_PHASE_NS && tid != CBTM_STAT_FRAME) pub.ctl_stats[tid] = 0;
     }
     __syncwarp();
     if (tid == 0) *pub.seq_frame += 1;
@@ -110,6 +112,50 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
                      smem_u32(dst)),
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
+}
+
+// Levels above `cnt` subtree roots (counters[cnt .. 2 cnt), cnt a power of two >= 2),
+// built by the last CTA to arrive (ticket; only thread 0 fences -- the fence is
+// cumulative over the preceding barrier).  Binary heap in shared memory (`heap`,
+// 2 * cnt words): coalesced L2 loads of the roots issued eight at a time per
+// thread so they overlap, log2(cnt) levels in shared memory, one coalesced
+// copy-out of all internal nodes (walking the levels through L2 instead costs a
+// round trip per level).  All nb CTAs must call it.
+__device__ __forceinline__ void finish_upper_tree(uint32_t *counters, uint32_t cnt, unsigned *ticket,
+                                                  const ReducePublish &pub, uint32_t *heap, bool *is_last,
+                                                  uint32_t nb)
+{
+    const int t = threadIdx.x;
+    __syncthreads();
+    if (t == 0) {
+        __threadfence();
+        *is_last = atomicAdd(ticket, 1u) == nb - 1;
+    }
+    __syncthreads();
+    if (!*is_last) return;
+    __threadfence();
+    for (uint32_t base = 0; base < cnt; base += 8 * RED_THREADS) {
+        uint32_t r[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t i = base + u * RED_THREADS + t;
+            r[u] = i < cnt ? __ldcg(&counters[cnt + i]) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t i = base + u * RED_THREADS + t;
+            if (i < cnt) heap[cnt + i] = r[u];
+        }
+    }
+    __syncthreads();
+    for (uint32_t w = cnt >> 1; w >= 1; w >>= 1) {
+        for (uint32_t i = t; i < w; i += RED_THREADS) heap[w + i] = heap[2 * (w + i)] + heap[2 * (w + i) + 1];
+        __syncthreads();
+    }
+    for (uint32_t i = 1 + t; i < cnt; i += RED_THREADS) counters[i] = heap[i];
+    if (t == 0) *ticket = 0;
+    publish_frame(pub, heap[1], t);
+    __syncthreads();
 }
 
 // Per-CTA state of the TMA ring that survives across frames of a persistent
@@ -229,44 +275,7 @@ __device__ __forceinline__ void reduce_phase(const uint8_t *bits, uint32_t *coun
         return;
     }
 
-    // ---- levels above the tile roots: last CTA standing ----
-    __syncthreads();
-    if (t == 0) {
-        __threadfence();
-        *rr.is_last = atomicAdd(ticket, 1u) == nb - 1;
-    }
-    __syncthreads();
-    if (!*rr.is_last) return;
-    __threadfence();
-
-    // Upper tree as a binary heap in the (now idle) ring: coalesced L2 loads of the
-    // tile roots, issued eight at a time per thread so they overlap; log2(cnt)
-    // levels in shared memory; one coalesced copy-out of all internal nodes.
-    // (Walking the levels through L2 instead costs a round trip per level.)
-    uint32_t *heap = reinterpret_cast<uint32_t *>(rr.ring); // 2 * cnt words <= stages * 16 KB
-    const uint32_t cnt = n_tiles;                           // power of two, 2 .. 8192
-    for (uint32_t base = 0; base < cnt; base += 8 * RED_THREADS) {
-        uint32_t r[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const uint32_t i = base + u * RED_THREADS + t;
-            r[u] = i < cnt ? __ldcg(&counters[cnt + i]) : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const uint32_t i = base + u * RED_THREADS + t;
-            if (i < cnt) heap[cnt + i] = r[u];
-        }
-    }
-    __syncthreads();
-    for (uint32_t w = cnt >> 1; w >= 1; w >>= 1) {
-        for (uint32_t i = t; i < w; i += RED_THREADS) heap[w + i] = heap[2 * (w + i)] + heap[2 * (w + i) + 1];
-        __syncthreads();
-    }
-    for (uint32_t i = 1 + t; i < cnt; i += RED_THREADS) counters[i] = heap[i];
-    if (t == 0) *ticket = 0;
-    publish_frame(pub, heap[1], t);
-    __syncthreads();
+    finish_upper_tree(counters, n_tiles, ticket, pub, reinterpret_cast<uint32_t *>(rr.ring), rr.is_last, nb);
 }
 
 __global__ void __launch_bounds__(RED_THREADS)
@@ -280,6 +289,121 @@ k_sum_reduce(const uint8_t *bits, uint32_t *counters, int lc, uint64_t total_byt
     ReduceRing rr{dyn_smem, full, wroot, &is_last, stages, 0};
     reduce_ring_init(rr);
     reduce_phase(bits, counters, lc, total_bytes, n_tiles, ticket, pub, rr, blockIdx.x, gridDim.x);
+}
+
+// ---------------------------------------------------------------------------
+// Incremental sum reduction (pipeline stage 9 inside a frame).  phase_apply
+// marks the leaf block of every bit it flips in a byte map (plain stores: no
+// read-modify-write, any number of writers); here the marked blocks recount
+// their 128-byte line and every level above the leaf blocks is rebuilt:
+// N/1024 counters + N/1024 marks in, as many counters out, plus 128 bytes per
+// touched block, instead of a pass over the whole bitfield (D = 26: ~0.4 MB
+// instead of 8 MB; the cost no longer grows with the bitfield).  A tile is 1024
+// leaf counters: a thread owns four (one 128-bit load) and with them two nodes
+// of level Lc-1 and one of Lc-2; five shuffle butterflies and one CTA barrier
+// give the other eight levels of the tile, as in reduce_phase.  The levels above
+// the tile roots (6 at D = 26) are not rebuilt: each tile adds the change of its
+// root to its ancestors with atomics, so there is no last-CTA pass, no ticket
+// and no fence on the frame's critical path.  Untouched tiles write nothing.
+// ---------------------------------------------------------------------------
+constexpr int UP_TILE = 1024;
+
+__device__ __forceinline__ uint32_t recount_block(const uint64_t *bits, uint32_t block)
+{
+    const uint4 *line = reinterpret_cast<const uint4 *>(bits) + (size_t)block * 8;
+    uint4 x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = line[j];
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c += popc128(x[j]);
+    return c;
+}
+
+__device__ __forceinline__ void upper_reduce_phase(const uint64_t *bits, uint8_t *dirty, uint32_t *counters,
+                                                   int lc, uint32_t (*wroot)[RED_THREADS / 32], uint32_t bid,
+                                                   uint32_t nb)
+{
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t nblocks = 1u << lc;
+    const uint32_t n_tiles = nblocks > (uint32_t)UP_TILE ? nblocks / UP_TILE : 1u;
+    const int top = lc > 10 ? lc - 10 : 0; // level of the tile roots
+    auto put = [&](int lvl, uint32_t pos, uint32_t val) {
+        if (lvl >= 0 && pos < (1u << lvl)) counters[(1u << lvl) + pos] = val;
+    };
+    uint32_t k = 0;
+    for (uint32_t tile = bid; tile < n_tiles; tile += nb, ++k) {
+        const uint32_t first = tile * UP_TILE + 4u * t;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        uint32_t d4 = 0, old_root = 0;
+        if (first + 4u <= nblocks) {
+            v = *reinterpret_cast<const uint4 *>(counters + nblocks + first);
+            d4 = *reinterpret_cast<const uint32_t *>(dirty + first);
+        } else if (first < nblocks) { // pools of 1 or 2 leaf blocks
+            v.x = counters[nblocks + first];
+            d4 = dirty[first];
+            if (first + 1 < nblocks) {
+                v.y = counters[nblocks + first + 1];
+                d4 |= (uint32_t)dirty[first + 1] << 8;
+            }
+        }
+        // the tile root as the levels above still see it (rewritten below by this same thread)
+        if (n_tiles > 1 && t == 0) old_root = counters[(1u << top) + tile];
+        if (d4) { // leaf blocks touched by this frame recount their line
+            if (d4 & 0x000000ffu) counters[nblocks + first] = v.x = recount_block(bits, first);
+            if (d4 & 0x0000ff00u) counters[nblocks + first + 1] = v.y = recount_block(bits, first + 1);
+            if (d4 & 0x00ff0000u) counters[nblocks + first + 2] = v.z = recount_block(bits, first + 2);
+            if (d4 & 0xff000000u) counters[nblocks + first + 3] = v.w = recount_block(bits, first + 3);
+            if (first + 4u <= nblocks)
+                *reinterpret_cast<uint32_t *>(dirty + first) = 0u;
+            else {
+                dirty[first] = 0;
+                if (first + 1 < nblocks) dirty[first + 1] = 0;
+            }
+        }
+        // a tile without a touched block keeps all its counters
+        if (!__syncthreads_or(d4 != 0)) continue;
+        const uint32_t a0 = v.x + v.y, a1 = v.z + v.w, c = a0 + a1;
+        put(lc - 1, tile * 512 + 2 * t, a0);
+        put(lc - 1, tile * 512 + 2 * t + 1, a1);
+        put(lc - 2, tile * 256 + t, c);
+        const uint32_t l1 = c + __shfl_xor_sync(FULL_MASK, c, 1);
+        const uint32_t l2 = l1 + __shfl_xor_sync(FULL_MASK, l1, 2);
+        const uint32_t l3 = l2 + __shfl_xor_sync(FULL_MASK, l2, 4);
+        const uint32_t l4 = l3 + __shfl_xor_sync(FULL_MASK, l3, 8);
+        const uint32_t l5 = l4 + __shfl_xor_sync(FULL_MASK, l4, 16);
+        if ((lane & 1) == 0) put(lc - 3, tile * 128 + warp * 16 + (lane >> 1), l1);
+        else if ((lane & 3) == 1) put(lc - 4, tile * 64 + warp * 8 + (lane >> 2), l2);
+        else if ((lane & 7) == 3) put(lc - 5, tile * 32 + warp * 4 + (lane >> 3), l3);
+        else if ((lane & 15) == 7) put(lc - 6, tile * 16 + warp * 2 + (lane >> 4), l4);
+        else if (lane == 15) put(lc - 7, tile * 8 + warp, l5);
+        if (lane == 0) wroot[k & 1][warp] = l5;
+        __syncthreads();
+        if (warp == 0 && lane < 7) {
+            const uint32_t *w = wroot[k & 1];
+            if (lane < 4) put(lc - 8, tile * 4 + lane, w[2 * lane] + w[2 * lane + 1]);
+            else if (lane < 6) {
+                const int q = (lane - 4) * 4;
+                put(lc - 9, tile * 2 + (lane - 4), w[q] + w[q + 1] + w[q + 2] + w[q + 3]);
+            } else
+                put(lc - 10, tile, w[0] + w[1] + w[2] + w[3] + w[4] + w[5] + w[6] + w[7]);
+        }
+        if (n_tiles > 1 && t == 0) { // the levels above the tile roots take the tile's delta
+            const uint32_t *w = wroot[k & 1];
+            const uint32_t delta = w[0] + w[1] + w[2] + w[3] + w[4] + w[5] + w[6] + w[7] - old_root;
+            if (delta) {
+                uint32_t idx = tile >> 1;
+                for (int l = top - 1; l >= 0; --l, idx >>= 1) atomicAdd(&counters[(1u << l) + idx], delta);
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(RED_THREADS)
+k_upper_reduce(const uint64_t *bits, uint8_t *dirty, uint32_t *counters, int lc)
+{
+    __shared__ uint32_t wroot[2][RED_THREADS / 32];
+    upper_reduce_phase(bits, dirty, counters, lc, wroot, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -400,7 +524,8 @@ __device__ __forceinline__ void fill_run_lines(int32_t *out, uint32_t first, uin
 
 __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32_t *counters, int depth,
                                             int32_t *cache_live, int32_t *cache_free, uint32_t *dispatch,
-                                            int32_t (*stage)[IDX_STAGE_WORDS], uint32_t bid, uint32_t nb)
+                                            uint32_t *reset_cmds, int32_t (*stage)[IDX_STAGE_WORDS],
+                                            uint32_t bid, uint32_t nb)
 {
     const Geo g = make_geo(depth);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -443,6 +568,8 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
 
             if (cnt == 0 || cnt == g.span) { // uniform block: no expansion needed
                 fill_run_lines(cnt ? cache_live : cache_free, cnt ? ones_before : zeros_before, g.span, base, lane);
+                if (cnt && reset_cmds)
+                    for (uint32_t e = lane; e < g.span; e += 32) reset_cmds[(uint32_t)base + e] = 0u;
                 continue;
             }
 
@@ -461,9 +588,10 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
                     if (word == 0u && !want_free) continue;
                     const uint32_t r1 = __popc(word & lane_lt);
                     const int32_t slot = base + w * 32 + lane;
-                    if ((word >> lane) & 1u)
+                    if ((word >> lane) & 1u) {
                         st[p1 + r1] = slot;
-                    else if (want_free)
+                        if (reset_cmds) reset_cmds[slot] = 0u; // stage 3 (kernels.py:256-259)
+                    } else if (want_free)
                         st[p0 + (uint32_t)lane - r1] = slot;
                     const uint32_t c = __popc(word);
                     p1 += c;
@@ -479,9 +607,10 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
                     const uint32_t r1 = __popc(word & lane_lt);
                     const int32_t slot = base + (int32_t)(w * 32u) + lane;
                     if ((uint32_t)lane < valid) {
-                        if ((word >> lane) & 1u)
+                        if ((word >> lane) & 1u) {
                             st[p1 + r1] = slot;
-                        else if (want_free)
+                            if (reset_cmds) reset_cmds[slot] = 0u;
+                        } else if (want_free)
                             st[p0 + (uint32_t)lane - r1] = slot;
                     }
                     const uint32_t c = __popc(word);
@@ -500,10 +629,11 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
 
 __global__ void __launch_bounds__(IDX_WARPS * 32)
 k_index(const uint32_t *bits32, const uint32_t *counters, int depth, int32_t *cache_live,
-        int32_t *cache_free, uint32_t *dispatch)
+        int32_t *cache_free, uint32_t *dispatch, uint32_t *reset_cmds)
 {
     __shared__ __align__(16) int32_t stage[IDX_WARPS][IDX_STAGE_WORDS];
-    index_phase(bits32, counters, depth, cache_live, cache_free, dispatch, stage, blockIdx.x, gridDim.x);
+    index_phase(bits32, counters, depth, cache_live, cache_free, dispatch, reset_cmds, stage, blockIdx.x,
+                gridDim.x);
 }
 
 // ---------------------------------------------------------------------------

@@ -11,20 +11,41 @@
 //              needs in rank order  ==  every rank before the first overflow
 //              i0 is accepted; from i0 on a first-fit walk accepts any later
 //              rank whose need still fits the remaining room (room < 187, so at
-//              most 93 acceptances; k_admit does this in one CTA)
+//              most 93 acceptances)
 //   placement  rank i with n_alloc_i slots receives the free ranks
 //              [T - incl_i, T - incl_i + n_alloc_i), incl = inclusive scan of
 //              n_alloc, T = total admitted reservation
 //
-// Phases of one frame, each a __device__ function over virtual CTA ids (bid of nb):
-//   index -> classify -> admit (1 CTA) -> scatter -> agree -> alloc_scan (1 CTA)
-//   -> reserve -> apply -> sum reduction (its last CTA also publishes the stats)
+// A frame is latency bound: a few MB of traffic, but every pass is a chain of
+// dependent steps (measured on B200, benchmarks/latency_probe.cu: L2 load
+// 160 ns, returning atomic 255 ns, CTA barrier ~65 ns, a flag seen by another
+// SM 430 ns, grid barrier 1.2 us).  What matters is the number of device-wide
+// joins and of single-CTA passes between them:
+//
+//   P1 index    stages 1-3: active list by stream compaction, command reset
+//   P2 classify stage 4: verdicts and reservation needs.  If even the worst
+//               case n * (3 * max_depth + 4) fits the free count -- always true
+//               for a pool sized like the paper's -- nothing can be rejected:
+//               chunks scatter their commands right away and the total T is one
+//               fire-and-forget atomic per chunk; the otherwise idle "admin" CTA
+//               waits for the last of them and builds the free-rank window table
+//               while the others are still walking split chains.
+//               Otherwise (pool under reservation pressure): P2b, one CTA scans
+//               the chunk needs, finds the first rejected rank and runs the
+//               first-fit tail; P2c scatters what was admitted.
+//   P3 agree    stage 5a: merge agreement snapshot, allocation count per chunk
+//   P4 reserve  stage 5b: every CTA sums the chunk counts before its chunk
+//               (a redundant range sum instead of a single-CTA scan phase) and
+//               hands out the free slots
+//   P5 apply    stages 6-8 fused; touched leaf blocks marked in a byte map
+//   P6 reduce   stage 9: marked leaf blocks recount their line, the levels up to
+//               the tile roots are rebuilt, the few levels above receive each
+//               tile's delta by atomics (no last-CTA pass, no fences)
+//
 // They run either as ONE persistent cooperative kernel (k_frames: phases
-// separated by grid barriers, any number of frames per launch -- a frame is
-// latency bound, so not paying a launch ramp and drain per phase is what
-// matters) or as one kernel per phase (k_<phase> wrappers: the staged path used
-// for the python-callable verdict source, for per-stage profiling and as the
-// fallback where cooperative launch is unavailable).
+// separated by grid barriers, any number of frames per launch) or as one kernel
+// per phase (k_<phase> wrappers: the staged path, used for per-stage profiling
+// and where cooperative launch is unavailable).
 #pragma once
 
 #include <cooperative_groups.h>
@@ -35,7 +56,6 @@
 namespace cbtm {
 
 constexpr int TAIL_MAX = 96;
-constexpr int ADMIT_THREADS = 1024; // standalone single-CTA kernels; 256 inside k_frames
 constexpr int MAX_SEQ_FRAMES = 4096;
 constexpr int WIN_MAX = 4096;       // leaf blocks covered by the free-rank window table
 
@@ -45,12 +65,15 @@ struct Control {
     int64_t i0;         // first rank rejected by admission (n if none)
     int32_t tail_count;
     uint32_t seq_frame; // index into prm_seq for sequence runs
+    unsigned long long need_total; // fast path: warps done << 40 | sum of their needs (zero between frames)
     int32_t tail_idx[TAIL_MAX];
-    uint32_t win_lo; // first leaf block of the free-rank window [T - A, T)
+    uint32_t win_lo; // first leaf block of the free-rank window table
     uint32_t win_n;  // leaf blocks in the window table (0: table not built, descend)
-    unsigned long long phase_t[CBTM_STAT_PHASES + 1]; // %globaltimer at the start of each phase
+    unsigned long long phase_t[2][CBTM_STAT_PHASES + 1]; // %globaltimer at the start of each phase, by frame parity
     int64_t stats[CBTM_STATS_WORDS];
 };
+
+constexpr int NEED_TOTAL_SHIFT = 40; // sum of needs < 2^30 * 187 < 2^38; warps of the live ranks < 2^24 on the fast path
 
 struct Workspace {
     uint8_t *need8;   // [N] by live rank: slots to reserve (0 = no command)
@@ -59,12 +82,12 @@ struct Workspace {
     int32_t *j4s;     // [N] by live rank: fourth member of a valid quad merge configuration
     int32_t *merge_ref; // [N] by slot: -1, or for a member of an agreed merge 2 * owner slot + (1 if the
                         // member sits in the pair opposite to the owner's, i.e. its parent is reserved[owner][1])
-    uint32_t *chunk_need;
-    uint64_t *chunk_need_off;
-    uint32_t *chunk_alloc;
-    uint64_t *chunk_alloc_off;
-    uint8_t *chunk_minneed;
+    uint32_t *chunk_need;     // [N/256] reservation need of each chunk of 256 live ranks
+    uint64_t *chunk_need_off; // [N/256] exclusive scan of chunk_need (pressure path only)
+    uint8_t *chunk_minneed;   // [N/256] smallest non-zero need of the chunk (255: none)
+    uint32_t *chunk_alloc;    // [N/256] slots allocated by each chunk
     uint32_t *win_prefix; // [WIN_MAX + 1] free ranks before each leaf block of the window
+    uint8_t *dirty;       // [N/1024] leaf blocks whose bits changed since the last reduction
     Control *ctl;
     double *prm_seq;  // [MAX_SEQ_FRAMES * 23]
     unsigned *ticket; // first word of the workspace: k_sum_reduce's CTA ticket
@@ -94,10 +117,10 @@ inline size_t carve_workspace(void *base, int depth, Workspace *ws)
     w.merge_ref = (int32_t *)take(4 * N);
     w.chunk_need = (uint32_t *)take(4 * nch);
     w.chunk_need_off = (uint64_t *)take(8 * nch);
-    w.chunk_alloc = (uint32_t *)take(4 * nch);
-    w.chunk_alloc_off = (uint64_t *)take(8 * nch);
     w.chunk_minneed = (uint8_t *)take(nch);
+    w.chunk_alloc = (uint32_t *)take(4 * nch);
     w.win_prefix = (uint32_t *)take(4 * (WIN_MAX + 1));
+    w.dirty = (uint8_t *)take(N >> LEAF_LOG2 ? N >> LEAF_LOG2 : 1);
     if (ws) *ws = w;
     return off;
 }
@@ -112,6 +135,14 @@ struct FrameArgs {
     int32_t pad_;
     double prm[CBTM_PRM_WORDS];
 };
+
+// No admission can fail when even the worst case fits: every live bisector asking
+// for the deepest split's reservation (kernels.py:279-288).  CTA- and grid-uniform.
+__device__ __forceinline__ bool fits_a_priori(const cbtm_pool &p, uint32_t n)
+{
+    const uint64_t F = ((uint64_t)1 << p.depth) - n;
+    return (uint64_t)n * (uint64_t)(3 * p.max_depth + 4) <= F;
+}
 
 // ---------------------------------------------------------------------------
 // merge configuration (kernels.py:112-191)
@@ -181,71 +212,265 @@ __device__ __forceinline__ bool wants_only_merge(uint32_t cmd)
 }
 
 // ---------------------------------------------------------------------------
-// stage 3 + 4a: reset commands, evaluate verdicts, compute each rank's
-// reservation need (3d+4 for a split, 2 for a valid merge, 0 otherwise).
+// start of a frame without an index phase (cbtm_update_finish: the caller ran
+// stages 1-2 and evaluated its verdicts on the host): stage 3 on its own.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void phase_classify(const FrameArgs &a, int8_t *verdict_out, uint32_t bid, uint32_t nb)
+__device__ __forceinline__ void phase_reset(const FrameArgs &a, uint32_t bid, uint32_t nb)
+{
+    const cbtm_pool &p = a.pool;
+    const uint32_t n = p.counters[1];
+    for (uint64_t i = bid * (uint64_t)CHUNK + threadIdx.x; i < n; i += (uint64_t)nb * CHUNK)
+        p.commands[p.cache_live[i]] = 0; // kernels.py:256-259
+}
+
+// ---------------------------------------------------------------------------
+// verdict sources (pipeline.py:87-119, lod.py:177-269)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int verdict_of(const FrameArgs &a, const double *prm, uint64_t id, uint32_t i)
+{
+    const cbtm_pool &p = a.pool;
+    switch (a.vmode) {
+    case CBTM_VERDICT_CONST: return a.vvalue;
+    case CBTM_VERDICT_UNIFORM: return depth_of(id, p.rank) < a.vvalue ? 1 : 0;
+    case CBTM_VERDICT_LOD: return lod_verdict(id, p.rank, p.max_depth, a.root_tris, prm);
+    default: return a.vexplicit[i];
+    }
+}
+
+__device__ __forceinline__ void load_prm(const FrameArgs &a, double *prm)
+{
+    if (a.vmode == CBTM_VERDICT_LOD) {
+        if (threadIdx.x < CBTM_PRM_WORDS)
+            prm[threadIdx.x] = a.use_prm_seq
+                                   ? a.ws.prm_seq[(size_t)CBTM_PRM_WORDS * a.ws.ctl->seq_frame + threadIdx.x]
+                                   : a.prm[threadIdx.x];
+        __syncthreads();
+    }
+}
+
+// standalone (KernelDecide.fill): no side effects on the pool
+__global__ void __launch_bounds__(CHUNK)
+k_classify(const __grid_constant__ FrameArgs a, int8_t *verdict_out)
+{
+    __shared__ double prm[CBTM_PRM_WORDS];
+    const cbtm_pool &p = a.pool;
+    const uint32_t n = p.counters[1];
+    load_prm(a, prm);
+    for (uint64_t i = blockIdx.x * (uint64_t)CHUNK + threadIdx.x; i < n; i += (uint64_t)gridDim.x * CHUNK)
+        verdict_out[i] = (int8_t)verdict_of(a, prm, p.ids[p.cache_live[i]], (uint32_t)i);
+}
+
+// Leaf block holding the free (unset) rank `rank` and the number of free slots
+// before that block.  One warp descends the counter heap five levels per step:
+// the 32 descendants of a node five levels down are contiguous in the heap, so
+// a step is one coalesced load, a warp scan and a ballot (4 round trips for
+// D = 26 instead of 16 dependent loads).
+__device__ __forceinline__ void warp_find_free_block(const uint32_t *counters, const Geo &g, uint32_t rank,
+                                                     uint32_t &block, uint32_t &free_before)
+{
+    const int lane = threadIdx.x & 31;
+    uint32_t idx = 0, before = 0; // node idx of level l
+    int l = 0;
+    while (l < g.lc) {
+        const int s = g.lc - l < 5 ? g.lc - l : 5;
+        const uint32_t fan = 1u << s;
+        const uint32_t child_span = (uint32_t)(g.n >> (l + s));
+        uint32_t z = 0;
+        if ((uint32_t)lane < fan) z = child_span - counters[(1u << (l + s)) + (idx << s) + lane];
+        const uint32_t incl = warp_inclusive_scan(z);
+        const unsigned hit = __ballot_sync(FULL_MASK, (uint32_t)lane < fan && incl > rank);
+        const int child = hit ? __ffs(hit) - 1 : (int)fan - 1;
+        const uint32_t excl = __shfl_sync(FULL_MASK, incl - z, child);
+        rank -= excl;
+        before += excl;
+        idx = (idx << s) + child;
+        l += s;
+    }
+    block = idx;
+    free_before = before;
+}
+
+// Same search by a whole CTA, eight levels per step (the 256 descendants of a
+// node eight levels down are contiguous): two round trips for D = 26.
+// scratch: 32 words, out: 2 words of shared memory.
+__device__ __forceinline__ void cta_find_free_block(const uint32_t *counters, const Geo &g, uint32_t rank,
+                                                    uint32_t *scratch, uint32_t *out, uint32_t &block,
+                                                    uint32_t &free_before)
+{
+    const int tid = threadIdx.x;
+    uint32_t idx = 0, before = 0;
+    int l = 0;
+    while (l < g.lc) {
+        const int s = g.lc - l < 8 ? g.lc - l : 8;
+        const uint32_t fan = 1u << s;
+        const uint32_t child_span = (uint32_t)(g.n >> (l + s));
+        const uint32_t z = (uint32_t)tid < fan ? child_span - counters[(1u << (l + s)) + (idx << s) + tid] : 0u;
+        uint32_t total;
+        const uint32_t incl = block_inclusive_scan<CHUNK>(z, scratch, &total);
+        if ((uint32_t)tid == fan - 1) { // default: the last child (rank beyond the free count)
+            out[0] = fan - 1;
+            out[1] = incl - z;
+        }
+        __syncthreads();
+        if ((uint32_t)tid < fan && incl > rank && incl - z <= rank) {
+            out[0] = (uint32_t)tid;
+            out[1] = incl - z;
+        }
+        __syncthreads();
+        const uint32_t child = out[0], excl = out[1];
+        __syncthreads();
+        rank -= excl;
+        before += excl;
+        idx = (idx << s) + child;
+        l += s;
+    }
+    block = idx;
+    free_before = before;
+}
+
+// The table that lets the reserve phase resolve free ranks without a tree
+// descent: all allocations of a frame draw from ONE interval of free ranks
+// [T - A, T) which lives in a short run of leaf blocks ending at the block of
+// free rank T - 1.  A is not known yet when T is, so the table is anchored at
+// the top: it covers the last WIN_MAX leaf blocks up to that one;
+// win_prefix[j] = free slots before leaf block win_lo + j.  (One CTA.)
+__device__ __forceinline__ void build_window_table(const FrameArgs &a, long long T)
+{
+    __shared__ uint32_t scratch[32];
+    __shared__ uint32_t s_out[2];
+    Control *ctl = a.ws.ctl;
+    const cbtm_pool &p = a.pool;
+    const Geo g = make_geo(p.depth);
+    const int tid = threadIdx.x;
+    if (tid == 0) ctl->win_n = 0;
+    if (T <= 0 || (p.flags & CBTM_POOL_FULL_FREE_CACHE)) return;
+    uint32_t hi, before_hi;
+    cta_find_free_block(p.counters, g, (uint32_t)(T - 1), scratch, s_out, hi, before_hi);
+    const uint32_t lo = hi + 1 > (uint32_t)WIN_MAX ? hi + 1 - WIN_MAX : 0u;
+    const uint32_t nbw = hi - lo + 1;
+    constexpr int PER = WIN_MAX / CHUNK;
+    const uint32_t per = (nbw + CHUNK - 1) / CHUNK; // <= PER
+    const uint32_t j0 = tid * per;
+    uint32_t z[PER], sum = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const uint32_t j = j0 + k;
+        z[k] = ((uint32_t)k < per && j < nbw) ? g.span - p.counters[g.nblocks + lo + j] : 0u;
+        sum += z[k];
+    }
+    uint32_t total;
+    const uint32_t incl = block_inclusive_scan<CHUNK>(sum, scratch, &total);
+    // free slots before block lo = (free before block hi) - (free in [lo, hi))
+    const uint32_t z_hi = g.span - p.counters[g.nblocks + hi];
+    const uint32_t base = before_hi - (total - z_hi);
+    uint32_t run = base + incl - sum;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const uint32_t j = j0 + k;
+        if ((uint32_t)k < per && j < nbw) a.ws.win_prefix[j] = run;
+        run += z[k];
+    }
+    if (tid == 0) {
+        a.ws.win_prefix[nbw] = base + total;
+        ctl->win_lo = lo;
+        ctl->win_n = nbw;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// P2 = stage 4: evaluate verdicts and compute each rank's reservation need
+// (3d+4 for a split, 2 for a valid merge, 0 otherwise).  Splits walk their
+// compatibility chain OR-ing edge-split bits (kernels.py:289-310); merges OR
+// their configuration bits (kernels.py:320-333).  OR is commutative, so the
+// final command words do not depend on scheduling.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void walk_split_chain(const cbtm_pool &p, int32_t s)
+{
+    // Pointer fields do not change during this phase, so the twin's operators
+    // are fetched while the atomic on `cur` is still in flight, and the twin's
+    // twin doubles as the next hop's twin: one dependent round trip per hop.
+    int32_t cur = s;
+    int32_t t = p.twins[cur];
+    for (int hops = 0;;) {
+        int32_t t_twin = -1, t_next = -1, t_prev = -1;
+        if (t >= 0) {
+            t_twin = p.twins[t];
+            t_next = p.nexts[t];
+            t_prev = p.prevs[t];
+        }
+        const uint32_t before = atomicOr(&p.commands[cur], CBTM_CMD_SPLIT_T);
+        if (before & CBTM_CMD_SPLIT_T) break; // another walker owns the rest of the chain
+        if (t < 0) break;
+        if (t_twin == cur) {
+            atomicOr(&p.commands[t], CBTM_CMD_SPLIT_T);
+            break;
+        }
+        if (t_next == cur)
+            atomicOr(&p.commands[t], CBTM_CMD_SPLIT_N);
+        else if (t_prev == cur)
+            atomicOr(&p.commands[t], CBTM_CMD_SPLIT_P);
+        else
+            break;
+        cur = t;
+        t = t_twin;
+        if (++hops > 70) break;
+    }
+}
+
+__device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t bid, uint32_t nb)
 {
     __shared__ double prm[CBTM_PRM_WORDS];
     __shared__ uint32_t wsum[CHUNK / 32], wmin[CHUNK / 32];
     const cbtm_pool &p = a.pool;
+    Control *ctl = a.ws.ctl;
     const uint32_t n = p.counters[1];
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
+    const bool fast = fits_a_priori(p, n); // nothing can be rejected: scatter right away
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    // per-frame counters start at zero (nothing accumulates before the next barrier)
-    if (!verdict_out && bid == 0 && tid < CBTM_STAT_PHASE_NS && tid != CBTM_STAT_FRAME) a.ws.ctl->stats[tid] = 0;
-
-    if (a.vmode == CBTM_VERDICT_LOD) {
-        if (tid < CBTM_PRM_WORDS)
-            prm[tid] = a.use_prm_seq ? a.ws.prm_seq[(size_t)CBTM_PRM_WORDS * a.ws.ctl->seq_frame + tid]
-                                     : a.prm[tid];
-        __syncthreads();
-    }
+    load_prm(a, prm);
 
     for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
         const uint32_t i = chunk * CHUNK + tid;
         uint32_t need = 0, mbits = 0;
+        int32_t s = -1;
         if (i < n) {
-            const int32_t s = p.cache_live[i];
+            s = p.cache_live[i];
             const uint64_t id = p.ids[s];
             // merge requests need these; fetched now so the latency hides behind the classifier
             const int32_t nx = p.nexts[s], pv = p.prevs[s];
-            int v;
-            switch (a.vmode) {
-            case CBTM_VERDICT_CONST: v = a.vvalue; break;
-            case CBTM_VERDICT_UNIFORM: v = depth_of(id, p.rank) < a.vvalue ? 1 : 0; break;
-            case CBTM_VERDICT_LOD: v = lod_verdict(id, p.rank, p.max_depth, a.root_tris, prm); break;
-            default: v = a.vexplicit[i]; break;
-            }
-            if (verdict_out) {
-                verdict_out[i] = (int8_t)v; // standalone verdict evaluation: no side effects
-            } else {
-                p.commands[s] = 0; // stage 3
-                if (v == 1) {
-                    const int d = depth_of(id, p.rank);
-                    if (d < p.max_depth) need = 3 * d + 4;
-                } else if (v == 2) {
-                    const MergeCfg c = merge_config(p, id, nx, pv);
-                    if (c.kind) {
-                        need = 2;
-                        mbits = CBTM_CMD_MERGE;
-                        uint64_t lowest = umin64(id, c.id_sib);
-                        if (c.kind == 2) {
-                            mbits |= CBTM_CMD_QUAD;
-                            lowest = umin64(lowest, c.id_oth);
-                            lowest = umin64(lowest, c.id_j4);
-                            a.ws.j4s[i] = c.j4;
-                        }
-                        if (lowest == id) mbits |= CBTM_CMD_OWNER;
+            const int v = verdict_of(a, prm, id, i);
+            if (v == 1) {
+                const int d = depth_of(id, p.rank);
+                if (d < p.max_depth) need = 3 * d + 4;
+            } else if (v == 2) {
+                const MergeCfg c = merge_config(p, id, nx, pv);
+                if (c.kind) {
+                    need = 2;
+                    mbits = CBTM_CMD_MERGE;
+                    uint64_t lowest = umin64(id, c.id_sib);
+                    if (c.kind == 2) {
+                        mbits |= CBTM_CMD_QUAD;
+                        lowest = umin64(lowest, c.id_oth);
+                        lowest = umin64(lowest, c.id_j4);
+                        a.ws.j4s[i] = c.j4;
                     }
+                    if (lowest == id) mbits |= CBTM_CMD_OWNER;
                 }
-                a.ws.need8[i] = (uint8_t)need;
-                a.ws.mbits8[i] = (uint8_t)mbits;
             }
+            a.ws.need8[i] = (uint8_t)need;
+            a.ws.mbits8[i] = (uint8_t)mbits;
         }
-        if (verdict_out) continue;
         uint32_t sum = warp_sum(need);
+        if (fast) {
+            // one fire-and-forget atomic per warp: warps-done count above, needs below
+            if (lane == 0) atomicAdd(&ctl->need_total, (unsigned long long)sum | (1ull << NEED_TOTAL_SHIFT));
+            if (need == 2)
+                atomicOr(&p.commands[s], mbits);
+            else if (need)
+                walk_split_chain(p, s);
+            continue;
+        }
         uint32_t mn = need ? need : 255u;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(FULL_MASK, mn, o));
@@ -266,11 +491,34 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, int8_t *verdi
         }
         __syncthreads();
     }
+
+    if (fast && bid == nb - 1) {
+        // admin: T = total need once every chunk has reported; then the window table
+        __shared__ unsigned long long s_total;
+        if (tid == 0) {
+            unsigned long long v;
+            do asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&ctl->need_total) : "memory");
+            while ((v >> NEED_TOTAL_SHIFT) < (unsigned long long)nch * (CHUNK / 32));
+            const unsigned long long total = v & ((1ull << NEED_TOTAL_SHIFT) - 1);
+            s_total = total;
+            ctl->need_total = 0; // nobody adds any more this frame
+            ctl->n = n;
+            ctl->F = (int64_t)(((uint64_t)1 << p.depth) - n);
+            ctl->T = (int64_t)total;
+            ctl->i0 = n;
+            ctl->tail_count = 0;
+            ctl->stats[CBTM_STAT_LIVE_BEFORE] = n;
+            ctl->stats[CBTM_STAT_RESERVED] = (int64_t)total;
+        }
+        __syncthreads();
+        build_window_table(a, (long long)s_total);
+    }
 }
 
 // ---------------------------------------------------------------------------
-// stage 4b (one CTA): admission.  Scans the per-chunk needs, locates the first
-// overflowing rank i0 and runs the first-fit tail walk.
+// P2b (one CTA; only when the pool is too full for the a-priori bound):
+// admission.  Scans the per-chunk needs, locates the first overflowing rank i0,
+// runs the first-fit tail walk, then builds the window table.
 // ---------------------------------------------------------------------------
 template <int NT>
 __device__ __forceinline__ void phase_admit(const FrameArgs &a)
@@ -324,6 +572,8 @@ __device__ __forceinline__ void phase_admit(const FrameArgs &a)
             ctl->stats[CBTM_STAT_LIVE_BEFORE] = n;
             ctl->stats[CBTM_STAT_RESERVED] = (int64_t)total_need;
         }
+        __syncthreads();
+        build_window_table(a, (long long)total_need);
         return;
     }
 
@@ -403,8 +653,8 @@ __device__ __forceinline__ void phase_admit(const FrameArgs &a)
         __syncthreads();
     }
     __syncthreads();
+    const long long T = (long long)F - (long long)s_room;
     if (tid == 0) {
-        const int64_t T = (int64_t)F - (int64_t)s_room;
         ctl->n = n;
         ctl->F = (int64_t)F;
         ctl->T = T;
@@ -412,47 +662,11 @@ __device__ __forceinline__ void phase_admit(const FrameArgs &a)
         ctl->stats[CBTM_STAT_LIVE_BEFORE] = n;
         ctl->stats[CBTM_STAT_RESERVED] = T;
     }
+    __syncthreads();
+    build_window_table(a, T);
 }
 
-// ---------------------------------------------------------------------------
-// stage 4c: scatter the admitted commands.  Splits walk their compatibility
-// chain OR-ing edge-split bits (kernels.py:289-310); merges OR their
-// configuration bits (kernels.py:320-333).  OR is commutative, so the final
-// command words do not depend on scheduling.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void walk_split_chain(const cbtm_pool &p, int32_t s)
-{
-    // Pointer fields do not change during this phase, so the twin's operators
-    // are fetched while the atomic on `cur` is still in flight, and the twin's
-    // twin doubles as the next hop's twin: one dependent round trip per hop.
-    int32_t cur = s;
-    int32_t t = p.twins[cur];
-    for (int hops = 0;;) {
-        int32_t t_twin = -1, t_next = -1, t_prev = -1;
-        if (t >= 0) {
-            t_twin = p.twins[t];
-            t_next = p.nexts[t];
-            t_prev = p.prevs[t];
-        }
-        const uint32_t before = atomicOr(&p.commands[cur], CBTM_CMD_SPLIT_T);
-        if (before & CBTM_CMD_SPLIT_T) break; // another walker owns the rest of the chain
-        if (t < 0) break;
-        if (t_twin == cur) {
-            atomicOr(&p.commands[t], CBTM_CMD_SPLIT_T);
-            break;
-        }
-        if (t_next == cur)
-            atomicOr(&p.commands[t], CBTM_CMD_SPLIT_N);
-        else if (t_prev == cur)
-            atomicOr(&p.commands[t], CBTM_CMD_SPLIT_P);
-        else
-            break;
-        cur = t;
-        t = t_twin;
-        if (++hops > 70) break;
-    }
-}
-
+// P2c: scatter the admitted commands (pressure path)
 __device__ __forceinline__ void phase_scatter(const FrameArgs &a, uint32_t bid, uint32_t nb)
 {
     __shared__ int32_t tail[TAIL_MAX];
@@ -561,126 +775,44 @@ __device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t bid, ui
     }
 }
 
-// Leaf block holding the free (unset) rank `rank` and the number of free slots
-// before that block.  One warp descends the counter heap five levels per step:
-// the 32 descendants of a node five levels down are contiguous in the heap, so
-// a step is one coalesced load, a warp scan and a ballot (4 round trips for
-// D = 26 instead of 16 dependent loads).
-__device__ __forceinline__ void warp_find_free_block(const uint32_t *counters, const Geo &g, uint32_t rank,
-                                                     uint32_t &block, uint32_t &free_before)
+// sum of v[lo, hi) by the whole CTA (every thread gets it); scratch: CHUNK / 32 words
+__device__ __forceinline__ uint64_t cta_range_sum(const uint32_t *v, uint32_t lo, uint32_t hi, unsigned long long *scratch)
 {
-    const int lane = threadIdx.x & 31;
-    uint32_t idx = 0, before = 0; // node idx of level l
-    int l = 0;
-    while (l < g.lc) {
-        const int s = g.lc - l < 5 ? g.lc - l : 5;
-        const uint32_t fan = 1u << s;
-        const uint32_t child_span = (uint32_t)(g.n >> (l + s));
-        uint32_t z = 0;
-        if ((uint32_t)lane < fan) z = child_span - counters[(1u << (l + s)) + (idx << s) + lane];
-        const uint32_t incl = warp_inclusive_scan(z);
-        const unsigned hit = __ballot_sync(FULL_MASK, (uint32_t)lane < fan && incl > rank);
-        const int child = hit ? __ffs(hit) - 1 : (int)fan - 1;
-        const uint32_t excl = __shfl_sync(FULL_MASK, incl - z, child);
-        rank -= excl;
-        before += excl;
-        idx = (idx << s) + child;
-        l += s;
-    }
-    block = idx;
-    free_before = before;
-}
-
-// stage 5b (one CTA): exclusive scan of the per-chunk allocation counts, then the
-// table that lets k_reserve resolve its free ranks without a tree descent: all
-// allocations of a frame draw from ONE interval of free ranks [T - A, T), which
-// lives in a short run of leaf blocks; win_prefix[j] = free slots before leaf
-// block win_lo + j.
-template <int NT>
-__device__ __forceinline__ void phase_alloc_scan(const FrameArgs &a)
-{
-    __shared__ uint32_t scratch[32];
-    __shared__ unsigned long long s_carry;
-    __shared__ uint32_t s_blk[2], s_before[2];
-    Control *ctl = a.ws.ctl;
-    const cbtm_pool &p = a.pool;
-    const Geo g = make_geo(p.depth);
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const uint32_t n = (uint32_t)ctl->n;
-    const uint32_t nch = (n + CHUNK - 1) / CHUNK;
-    if (tid == 0) s_carry = 0;
+    unsigned long long acc = 0;
+    for (uint32_t j = lo + threadIdx.x; j < hi; j += CHUNK) acc += v[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, o);
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = acc;
     __syncthreads();
-    for (uint32_t base = 0; base < nch; base += NT) {
-        const uint32_t c = base + tid;
-        const uint32_t v = c < nch ? a.ws.chunk_alloc[c] : 0;
-        uint32_t total;
-        const uint32_t incl = block_inclusive_scan<NT>(v, scratch, &total);
-        const unsigned long long carry = s_carry;
-        if (c < nch) a.ws.chunk_alloc_off[c] = carry + incl - v;
-        __syncthreads();
-        if (tid == 0) s_carry = carry + total;
-        __syncthreads();
-    }
-    const long long A = (long long)s_carry;
-    const long long T = ctl->T;
-    if (tid == 0) {
-        ctl->A = A;
-        ctl->stats[CBTM_STAT_ALLOCATED] = A;
-        p.counter[0] = T - A; // reservation slack left in the counter (kernels.py:357)
-        ctl->win_n = 0;
-    }
-    if (A == 0 || (p.flags & CBTM_POOL_FULL_FREE_CACHE)) return;
-
-    // leaf blocks of the first and the last free rank of the window
-    if (warp < 2) {
-        uint32_t blk, before;
-        warp_find_free_block(p.counters, g, (uint32_t)(warp == 0 ? T - A : T - 1), blk, before);
-        if ((tid & 31) == 0) {
-            s_blk[warp] = blk;
-            s_before[warp] = before;
-        }
-    }
+    unsigned long long total = 0;
+#pragma unroll
+    for (int w = 0; w < CHUNK / 32; ++w) total += scratch[w];
     __syncthreads();
-    const uint32_t lo = s_blk[0], hi = s_blk[1];
-    const uint32_t nbw = hi - lo + 1;
-    if (nbw > (uint32_t)WIN_MAX) return; // fragmented pool: k_reserve descends per rank
-    if (tid == 0) s_carry = s_before[0];
-    __syncthreads();
-    for (uint32_t base = 0; base < nbw; base += NT) {
-        const uint32_t j = base + tid;
-        const uint32_t z = j < nbw ? g.span - p.counters[g.nblocks + lo + j] : 0;
-        uint32_t total;
-        const uint32_t incl = block_inclusive_scan<NT>(z, scratch, &total);
-        const unsigned long long carry = s_carry;
-        if (j < nbw) a.ws.win_prefix[j] = (uint32_t)(carry + incl - z);
-        __syncthreads();
-        if (tid == 0) s_carry = carry + total;
-        __syncthreads();
-    }
-    if (tid == 0) {
-        a.ws.win_prefix[nbw] = (uint32_t)s_carry;
-        ctl->win_lo = lo;
-        ctl->win_n = nbw;
-    }
+    return total;
 }
 
 // ---------------------------------------------------------------------------
-// stage 5c: hand out free slots.  Rank i owns free ranks [T - incl_i, ...):
+// P4 = stage 5b: hand out free slots.  Rank i owns free ranks [T - incl_i, ...):
 // windows are popped from the top of the reserved range exactly like the serial
-// atomic_sub of kernels.py:357-360.
-// ---------------------------------------------------------------------------
+// atomic_sub of kernels.py:357-360.  The exclusive prefix of a chunk is a range
+// sum over the chunk counts before it, computed redundantly by the CTA that
+// needs it (the counts of a frame are a few KB that every CTA reads from L2 in
+// one round trip) -- cheaper than a single-CTA scan phase between two barriers.
 // The 256 ranks of a chunk draw ONE contiguous interval of free ranks
 // [T - off - total, T - off), total <= 1024.  With the window table the CTA
 // expands the free bits of the few leaf blocks that hold that interval into
-// shared memory (a warp per leaf block, like k_index) and every thread then
-// just picks its slots; without it (fragmented pool) each thread descends.
+// shared memory (a warp per leaf block, like the index phase) and every thread
+// then just picks its slots; outside the table (fragmented pool) each thread
+// descends the tree.
+// ---------------------------------------------------------------------------
 __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t bid, uint32_t nb)
 {
     __shared__ uint32_t scratch[32];
+    __shared__ unsigned long long scratch64[CHUNK / 32];
     __shared__ int32_t slots[4 * CHUNK];
     __shared__ uint32_t s_j0;
     const cbtm_pool &p = a.pool;
-    const Control *ctl = a.ws.ctl;
+    Control *ctl = a.ws.ctl;
     const Geo g = make_geo(p.depth);
     const uint32_t n = (uint32_t)ctl->n;
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
@@ -689,30 +821,39 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t bid, 
     const uint32_t *win = a.ws.win_prefix;
     const uint32_t *bits32 = reinterpret_cast<const uint32_t *>(p.bits);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // one read per CTA, broadcast (the branch on win_n must be CTA-uniform)
-    __shared__ uint32_t s_win[2];
-    if (tid == 0) {
-        s_win[0] = ctl->win_n;
-        s_win[1] = ctl->win_lo;
-    }
-    __syncthreads();
-    const uint32_t win_n = s_win[0], win_lo = s_win[1];
+    const uint32_t win_n = ctl->win_n, win_lo = ctl->win_lo; // CTA-uniform: written before the last barrier
+    const uint32_t win_first = win_n ? win[0] : 0u;
+
+    long long off = 0;      // slots allocated by chunks [0, summed)
+    uint32_t summed = 0;
     for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
-        const uint32_t total_hint = a.ws.chunk_alloc[chunk];
-        if (total_hint == 0) continue;
+        const uint32_t total = a.ws.chunk_alloc[chunk];
+        if (total == 0) continue; // CTA-uniform
+        off += (long long)cta_range_sum(a.ws.chunk_alloc, summed, chunk, scratch64);
+        summed = chunk;
         const uint32_t i = chunk * CHUNK + tid;
         const uint32_t na = i < n ? a.ws.nalloc8[i] : 0;
-        uint32_t total;
-        const uint32_t incl = block_inclusive_scan<CHUNK>(na, scratch, &total);
-        const long long off = (long long)a.ws.chunk_alloc_off[chunk];
-        const long long base = T - (off + incl);
-        const bool coop = !full && win_n != 0;
+        uint32_t total_chk;
+        const uint32_t incl = block_inclusive_scan<CHUNK>(na, scratch, &total_chk);
+
+        const long long base = T - (off + incl); // this rank's first free rank
         const uint32_t lo_rank = (uint32_t)(T - off - total), hi_rank = (uint32_t)(T - off);
+        const bool coop = !full && win_n != 0 && lo_rank >= win_first;
         if (coop) {
-            // window block holding the lowest rank of the chunk
-            for (uint32_t j = tid; j < win_n; j += CHUNK)
-                if (win[j] <= lo_rank && lo_rank < win[j + 1]) s_j0 = j;
-            __syncthreads();
+            // window block holding the lowest rank of the chunk; windows sit near the top of the table
+            uint32_t top = win_n;
+            while (true) {
+                bool hit = false;
+                if ((uint32_t)tid < top) {
+                    const uint32_t j = top - 1 - tid;
+                    if (win[j] <= lo_rank && lo_rank < win[j + 1]) {
+                        s_j0 = j;
+                        hit = true;
+                    }
+                }
+                if (__syncthreads_or(hit) || top <= (uint32_t)CHUNK) break;
+                top -= CHUNK;
+            }
             for (uint32_t j = s_j0 + warp; j < win_n; j += CHUNK / 32) {
                 const uint32_t first = win[j]; // free rank of the block's first free slot
                 if (first >= hi_rank) break;
@@ -748,6 +889,14 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t bid, 
             }
         }
         __syncthreads(); // slots / s_j0 are reused by the next chunk
+    }
+    if (bid == nb - 1) { // totals of the allocation scan
+        const long long A = off + (long long)cta_range_sum(a.ws.chunk_alloc, summed, nch, scratch64);
+        if (tid == 0) {
+            ctl->A = A;
+            ctl->stats[CBTM_STAT_ALLOCATED] = A;
+            p.counter[0] = T - A; // reservation slack left in the counter (kernels.py:357)
+        }
     }
 }
 
@@ -823,6 +972,7 @@ struct Neighbour {
 struct ApplyCtx {
     const cbtm_pool &p;
     const int32_t *merge_ref;
+    uint8_t *dirty;
     uint32_t poison;
 };
 
@@ -913,14 +1063,23 @@ __device__ __forceinline__ void redirect_to(const cbtm_pool &p, const Neighbour 
     if (t.tw == old_slot) p.twins[t.slot] = new_slot;
 }
 
-__device__ __forceinline__ void set_live(uint32_t *bits32, int32_t slot)
+// Every flipped occupancy bit marks its leaf block in the dirty map, so the
+// frame's reduction recounts only the touched blocks (upper_reduce_phase).
+struct BitSink {
+    uint32_t *bits32;
+    uint8_t *dirty;
+};
+
+__device__ __forceinline__ void set_live(const BitSink &b, int32_t slot)
 {
-    atomicOr(&bits32[slot >> 5], 1u << (slot & 31));
+    atomicOr(&b.bits32[slot >> 5], 1u << (slot & 31));
+    b.dirty[(uint32_t)slot >> LEAF_LOG2] = 1;
 }
 
-__device__ __forceinline__ void set_free(uint32_t *bits32, int32_t slot)
+__device__ __forceinline__ void set_free(const BitSink &b, int32_t slot)
 {
-    atomicAnd(&bits32[slot >> 5], ~(1u << (slot & 31)));
+    atomicAnd(&b.bits32[slot >> 5], ~(1u << (slot & 31)));
+    b.dirty[(uint32_t)slot >> LEAF_LOG2] = 1;
 }
 
 // kernels.py:373-461 restated over the two halves of the bisector
@@ -978,7 +1137,7 @@ __device__ __forceinline__ void apply_split(ApplyCtx &cx, int32_t s, uint32_t sm
     if (!split_p && nb_p >= 0 && survives(tp)) redirect_to(p, tp, s, r4.x, E_NEXT);
 
     // stage 8
-    uint32_t *bits32 = reinterpret_cast<uint32_t *>(p.bits);
+    const BitSink bits32{reinterpret_cast<uint32_t *>(p.bits), cx.dirty};
     set_free(bits32, s);
     set_live(bits32, r4.x);
     set_live(bits32, r4.y);
@@ -1009,9 +1168,9 @@ __device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t bid, ui
     const int tid = threadIdx.x;
     if (tid < 5) acc[tid] = 0;
     __syncthreads();
-    ApplyCtx cx{p, a.ws.merge_ref, 0};
+    ApplyCtx cx{p, a.ws.merge_ref, a.ws.dirty, 0};
     uint32_t split_freed = 0, merge_freed = 0, split_alloc = 0, merge_alloc = 0;
-    uint32_t *bits32 = reinterpret_cast<uint32_t *>(p.bits);
+    const BitSink bits32{reinterpret_cast<uint32_t *>(p.bits), cx.dirty};
 
     for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
         const uint32_t i = chunk * CHUNK + tid;
@@ -1072,30 +1231,31 @@ __device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t bid, ui
 // ---------------------------------------------------------------------------
 // one kernel per phase (staged path)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(CHUNK)
-k_classify(const __grid_constant__ FrameArgs a, int8_t *verdict_out)
+__global__ void __launch_bounds__(CHUNK) k_reset(const __grid_constant__ FrameArgs a)
 {
-    phase_classify(a, verdict_out, blockIdx.x, gridDim.x);
+    phase_reset(a, blockIdx.x, gridDim.x);
 }
 
-__global__ void __launch_bounds__(ADMIT_THREADS) k_admit(const __grid_constant__ FrameArgs a)
+// fast path: the admin CTA waits for the other CTAs of the grid, which therefore
+// must all be resident (the host sizes this grid from the kernel's occupancy)
+__global__ void __launch_bounds__(CHUNK) k_classify_frame(const __grid_constant__ FrameArgs a)
 {
-    phase_admit<ADMIT_THREADS>(a);
+    phase_classify(a, blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(CHUNK) k_admit(const __grid_constant__ FrameArgs a)
+{
+    if (!fits_a_priori(a.pool, a.pool.counters[1])) phase_admit<CHUNK>(a);
 }
 
 __global__ void __launch_bounds__(CHUNK) k_scatter(const __grid_constant__ FrameArgs a)
 {
-    phase_scatter(a, blockIdx.x, gridDim.x);
+    if (!fits_a_priori(a.pool, (uint32_t)a.ws.ctl->n)) phase_scatter(a, blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(CHUNK) k_agree(const __grid_constant__ FrameArgs a)
 {
     phase_agree(a, blockIdx.x, gridDim.x);
-}
-
-__global__ void __launch_bounds__(ADMIT_THREADS) k_alloc_scan(const __grid_constant__ FrameArgs a)
-{
-    phase_alloc_scan<ADMIT_THREADS>(a);
 }
 
 __global__ void __launch_bounds__(CHUNK) k_reserve(const __grid_constant__ FrameArgs a)
@@ -1108,10 +1268,16 @@ __global__ void __launch_bounds__(CHUNK) k_apply(const __grid_constant__ FrameAr
     phase_apply(a, blockIdx.x, gridDim.x);
 }
 
+__global__ void __launch_bounds__(CHUNK) k_publish(const __grid_constant__ FrameArgs a, int64_t *stats_seq)
+{
+    const ReducePublish pub = {a.ws.ctl->stats, a.pool.stats, stats_seq, &a.ws.ctl->seq_frame, nullptr};
+    publish_frame(pub, a.pool.counters[1], threadIdx.x);
+}
+
 // ---------------------------------------------------------------------------
 // the persistent frame kernel: n_frames full updates in one cooperative launch
 // ---------------------------------------------------------------------------
-constexpr int FRAMES_DYN_SMEM = RED_MAX_STAGES * RED_TILE_BYTES; // 64 KB: index staging (36 KB) / TMA ring / upper-tree heap
+constexpr int FRAMES_DYN_SMEM = IDX_WARPS * IDX_STAGE_WORDS * 4; // 36 KB: index staging
 
 __global__ void __launch_bounds__(CHUNK, 2)
 k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, int do_index)
@@ -1119,61 +1285,55 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(128) uint8_t dyn_smem[];
-    __shared__ __align__(8) uint64_t full[RED_MAX_STAGES];
     __shared__ uint32_t wroot[2][RED_THREADS / 32];
-    __shared__ bool is_last;
 
     const cbtm_pool &p = a.pool;
+    Control *ctl = a.ws.ctl;
     const uint32_t bid = blockIdx.x, nb = gridDim.x;
     const Geo g = make_geo(p.depth);
-    const uint32_t n_tiles = g.nblocks > (uint32_t)RED_TILE_BLOCKS ? g.nblocks / RED_TILE_BLOCKS : 1u;
-    const uint64_t total_bytes = (uint64_t)bitfield_words(p.depth) * 8;
-    const uint32_t per_cta = (n_tiles + nb - 1) / nb;
-    ReduceRing rr{dyn_smem, full, wroot, &is_last,
-                  per_cta < (uint32_t)RED_MAX_STAGES ? (per_cta ? (int)per_cta : 1) : RED_MAX_STAGES, 0};
-    reduce_ring_init(rr);
-    const ReducePublish pub = {a.ws.ctl->stats, p.stats, stats_seq, &a.ws.ctl->seq_frame, a.ws.ctl->phase_t};
-    unsigned long long *stamp = (bid == 0 && threadIdx.x == 0) ? a.ws.ctl->phase_t : nullptr;
+    const bool stamper = bid == 0 && threadIdx.x == 0;
     int32_t *free_list = (p.flags & CBTM_POOL_FULL_FREE_CACHE) ? p.cache_free : nullptr;
 
     for (int f = 0; f < n_frames; ++f) {
+        unsigned long long *stamp = stamper ? ctl->phase_t[f & 1] : nullptr;
         if (stamp) stamp[0] = global_ns();
-        if (do_index) {
+        if (do_index)
             index_phase(reinterpret_cast<const uint32_t *>(p.bits), p.counters, p.depth, p.cache_live,
-                        free_list, p.dispatch, reinterpret_cast<int32_t(*)[IDX_STAGE_WORDS]>(dyn_smem), bid, nb);
+                        free_list, p.dispatch, p.commands,
+                        reinterpret_cast<int32_t(*)[IDX_STAGE_WORDS]>(dyn_smem), bid, nb);
+        else
+            phase_reset(a, bid, nb);
+        grid.sync();
+        if (stamp) stamp[1] = global_ns();
+        const bool fast = fits_a_priori(p, p.counters[1]); // grid-uniform
+        phase_classify(a, bid, nb);
+        grid.sync();
+        if (!fast) { // pool under reservation pressure: one CTA admits, then everybody scatters
+            if (bid == 0) phase_admit<CHUNK>(a);
+            grid.sync();
+            phase_scatter(a, bid, nb);
             grid.sync();
         }
-        if (stamp) stamp[1] = global_ns();
-        phase_classify(a, nullptr, bid, nb);
-        grid.sync();
         if (stamp) stamp[2] = global_ns();
-        if (bid == 0) phase_admit<CHUNK>(a);
-        grid.sync();
-        if (stamp) stamp[3] = global_ns();
-        phase_scatter(a, bid, nb);
-        grid.sync();
-        if (stamp) stamp[4] = global_ns();
         phase_agree(a, bid, nb);
         grid.sync();
-        if (stamp) stamp[5] = global_ns();
-        if (bid == 0) phase_alloc_scan<CHUNK>(a);
-        grid.sync();
-        if (stamp) stamp[6] = global_ns();
+        if (stamp) stamp[3] = global_ns();
         phase_reserve(a, bid, nb);
         grid.sync();
-        if (stamp) stamp[7] = global_ns();
+        if (stamp) stamp[4] = global_ns();
         phase_apply(a, bid, nb);
-        if (stamp) {
-            __threadfence(); // the publishing CTA reads the stamps after the next barrier
-        }
         grid.sync();
         if (stamp) {
-            stamp[8] = global_ns();
-            __threadfence();
+            stamp[5] = global_ns();
+            __threadfence(); // read by the publishing CTA after the next barrier
         }
-        reduce_phase(reinterpret_cast<const uint8_t *>(p.bits), p.counters, g.lc, total_bytes, n_tiles,
-                     a.ws.ticket, pub, rr, bid, nb);
+        upper_reduce_phase(p.bits, a.ws.dirty, p.counters, g.lc, wroot, bid, nb);
         grid.sync();
+        // the frame's counters go out while the next frame's index phase is already running
+        if (bid == nb - 1) {
+            const ReducePublish pub = {ctl->stats, p.stats, stats_seq, &ctl->seq_frame, ctl->phase_t[f & 1]};
+            publish_frame(pub, p.counters[1], threadIdx.x);
+        }
     }
 }
 
@@ -1238,9 +1398,10 @@ k_validate(const cbtm_pool p, int n_halfedges, unsigned long long *out)
 // ---------------------------------------------------------------------------
 __global__ void k_initialize(const cbtm_pool p, const int32_t *__restrict__ he_next,
                              const int32_t *__restrict__ he_prev,
-                             const int32_t *__restrict__ he_twin, int n_halfedges, Control *ctl,
-                             unsigned *ticket)
+                             const int32_t *__restrict__ he_twin, int n_halfedges, const Workspace ws)
 {
+    Control *ctl = ws.ctl;
+    unsigned *ticket = ws.ticket;
     const uint64_t N = (uint64_t)1 << p.depth;
     const uint64_t base = (uint64_t)1 << p.rank;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -1255,6 +1416,10 @@ __global__ void k_initialize(const cbtm_pool p, const int32_t *__restrict__ he_n
         reinterpret_cast<int4 *>(p.reserved)[s] = make_int4(-1, -1, -1, -1);
         p.cache_live[s] = -1;
         p.cache_free[s] = -1;
+    }
+    if (ws.dirty) {
+        const uint64_t nblk = N >> LEAF_LOG2 ? N >> LEAF_LOG2 : 1;
+        for (uint64_t b = gid; b < nblk; b += stride) ws.dirty[b] = 0;
     }
     const uint64_t words = bitfield_words(p.depth);
     for (uint64_t w = gid; w < words; w += stride) {
@@ -1273,6 +1438,7 @@ __global__ void k_initialize(const cbtm_pool p, const int32_t *__restrict__ he_n
             ctl->i0 = 0;
             ctl->tail_count = 0;
             ctl->seq_frame = 0;
+            ctl->need_total = 0;
             *ticket = 0;
             for (int k = 0; k < CBTM_STATS_WORDS; ++k) ctl->stats[k] = 0;
         }

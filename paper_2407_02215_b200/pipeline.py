@@ -48,7 +48,7 @@ class UpdateStats:
     stage_times_us: list = field(default_factory=lambda: [0] * 9)
     reserved_slots: int = 0   # T: slots reserved by admitted commands
     poison: int = 0           # fresh pointers that resolved to the poison -2
-    phase_ns: list = field(default_factory=lambda: [0] * 9)  # device ns per phase (_lib.PHASE_NAMES)
+    phase_ns: list = field(default_factory=lambda: [0] * 6)  # device ns per phase (_lib.PHASE_NAMES)
 
     @property
     def structural_ops(self) -> int:
@@ -64,16 +64,18 @@ class UpdateStats:
     @classmethod
     def from_device_words(cls, words, epoch: int, times=None) -> "UpdateStats":
         w = [int(x) for x in words]
-        if times is None and len(w) >= _lib.STAT_PHASE_NS + 9 and any(w[_lib.STAT_PHASE_NS:_lib.STAT_PHASE_NS + 9]):
+        np_ = len(_lib.PHASE_NAMES)
+        if times is None and len(w) >= _lib.STAT_PHASE_NS + np_ and any(w[_lib.STAT_PHASE_NS:_lib.STAT_PHASE_NS + np_]):
             # device-measured phase times (ns) folded onto the reference's nine stages:
-            # t2 cache pointers = index; t4 generate commands = classify + admit + scatter;
-            # t5 reserve = agree + alloc_scan + reserve; t6 = fused fill/neighbours/bitfield; t9 reduce
-            ph = w[_lib.STAT_PHASE_NS:_lib.STAT_PHASE_NS + 9]
+            # t2 cache pointers = index (also resets the commands, stage 3); t4 generate commands =
+            # classify + admission + scatter; t5 reserve = agreement + slot hand-out;
+            # t6 = fused fill/neighbours/bitfield; t9 = reduction (+ stats publish)
+            ph = w[_lib.STAT_PHASE_NS:_lib.STAT_PHASE_NS + np_]
             us = lambda *ks: sum(ph[k] for k in ks) // 1000  # noqa: E731
-            times = [0, us(0), 0, us(1, 2, 3), us(4, 5, 6), us(7), 0, 0, us(8)]
+            times = [0, us(0), 0, us(1), us(2, 3), us(4), 0, 0, us(5)]
             phase_ns = list(ph)
         else:
-            phase_ns = [0] * 9
+            phase_ns = [0] * np_
         return cls(phase_ns=phase_ns, epoch=epoch, live_before=w[6], live_after=w[7],
                    splits_applied=w[2], merges_applied=w[3],
                    splits_rejected_oom=w[0], merges_rejected_oom=w[1],
