@@ -50,6 +50,7 @@ extern "C" {
 #define CBTM_E_MODE 4      /* unknown verdict mode / flag */
 #define CBTM_E_RANGE 5     /* count / size argument out of range */
 #define CBTM_E_ALIGN 6     /* bits, reserved, cache_live, cache_free must be 16-byte aligned */
+#define CBTM_E_TIMEOUT 7   /* cbtm_wait_frame gave up */
 
 /* command-word bits (state.py:17-25) */
 #define CBTM_CMD_SPLIT_T 1u
@@ -84,6 +85,10 @@ enum {
     CBTM_STAT_ALLOCATED = 9, /* A: slots actually allocated              */
     CBTM_STAT_POISON = 10,   /* fresh pointers resolved to the poison -2 */
     CBTM_STAT_FRAME = 11,    /* frames applied to this pool so far       */
+    CBTM_STAT_SEQ = 31,      /* = CBTM_STAT_FRAME, but stored LAST: the other words are written, then a
+                              * system-scope fence, then this one -- so when cbtm_pool.stats points to
+                              * host-mapped pinned memory the host may poll this word (cbtm_wait_frame)
+                              * and then read the frame's counters without any stream synchronisation */
     /* words 16..21: device time of each phase of the frame in ns (persistent
      * frame kernel only; 0 on the staged path): index (stages 1-3), classify +
      * admission + command scatter (stage 4), merge agreement (stage 5a), slot
@@ -223,6 +228,14 @@ int cbtm_validate(const cbtm_pool *pool, int32_t n_halfedges, int64_t *out, uint
 int cbtm_update(const cbtm_pool *pool, const cbtm_verdict *verdict, uintptr_t stream);
 int cbtm_update_begin(const cbtm_pool *pool, uintptr_t stream);
 int cbtm_update_finish(const cbtm_pool *pool, const cbtm_verdict *verdict, uintptr_t stream);
+
+/* ---- host side of the zero-copy stats path (the one call that blocks, and the only one that
+ *      takes a HOST pointer to pool memory): spins until host_stats[CBTM_STAT_SEQ] >= frame, where
+ *      host_stats is the host address of a pinned, device-mapped buffer that was passed as
+ *      cbtm_pool.stats.  Replaces "copy the stats back + synchronise the stream" in
+ *      ParallelEngine.update (pipeline.py:303-322 reads its counters on the host after every
+ *      update).  Returns 0, or CBTM_E_TIMEOUT after timeout_ns. */
+int cbtm_wait_frame(const int64_t *host_stats, int64_t frame, uint64_t timeout_ns);
 
 /* ---- ParallelEngine.run_epochs / cmd_animate (pipeline.py:324-337,
  *      cli.py:226-231) for LOD sequences: n_frames updates back to back, no host

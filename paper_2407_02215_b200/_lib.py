@@ -19,6 +19,8 @@ LIB_PATH = os.path.join(_HERE, "libcbtm.so")
 PRM_WORDS = 23
 STATS_WORDS = 32
 STAT_PHASE_NS = 16
+STAT_FRAME = 11
+STAT_SEQ = 31
 PHASE_NAMES = ("index", "classify_admit_scatter", "agree", "reserve", "apply", "reduce_publish")
 MIN_DEPTH = 1
 MAX_DEPTH_ABI = 30
@@ -34,7 +36,8 @@ STAT_NAMES = ("oom_splits", "oom_merges", "split_freed", "merge_freed",
 
 _ERRORS = {1: "depth out of range", 2: "required pointer is NULL",
            3: "workspace too small", 4: "unknown verdict mode",
-           5: "argument out of range", 6: "buffer not 16-byte aligned"}
+           5: "argument out of range", 6: "buffer not 16-byte aligned",
+           7: "timed out waiting for the frame's stats"}
 
 
 class CbtmError(RuntimeError):
@@ -85,6 +88,7 @@ SIGNATURES = {
     "cbtm_update_begin": (C.c_int, [C.POINTER(CPool), _UP]),
     "cbtm_update_finish": (C.c_int, [C.POINTER(CPool), C.POINTER(CVerdict), _UP]),
     "cbtm_run_lod_sequence": (C.c_int, [C.POINTER(CPool), _P, _P, C.c_int32, _P, _UP]),
+    "cbtm_wait_frame": (C.c_int, [_P, _I64, C.c_uint64]),
 }
 
 _lib = None
@@ -143,7 +147,13 @@ def require_cuda(device=None):
 
 
 def stream_handle(device) -> int:
-    return int(torch().cuda.current_stream(device).cuda_stream)
+    """cudaStream_t of torch's current stream on `device` (the raw query is a
+    fraction of the cost of building a torch.cuda.Stream object every frame)."""
+    t = torch()
+    raw = getattr(t._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return int(raw(device.index if device.index is not None else t.cuda.current_device()))
+    return int(t.cuda.current_stream(device).cuda_stream)
 
 
 def ptr(tensor) -> int:

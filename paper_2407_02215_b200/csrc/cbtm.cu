@@ -4,6 +4,9 @@
 // Build (see paper_2407_02215_b200/build.py):
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false
 //        --shared -Xcompiler -fPIC -o libcbtm.so cbtm.cu
+#include <atomic>
+#include <chrono>
+
 #include "cbtm_frame.cuh"
 
 using namespace cbtm;
@@ -391,6 +394,23 @@ int cbtm_update(const cbtm_pool *pool, const cbtm_verdict *verdict, uintptr_t st
         return rc ? rc : finish_staged(a, nullptr, false, as_stream(stream));
     }
     return frames_launch(a, 1, nullptr, 1, grid, as_stream(stream));
+}
+
+int cbtm_wait_frame(const int64_t *host_stats, int64_t frame, uint64_t timeout_ns)
+{
+    if (!host_stats) return CBTM_E_NULL;
+    const volatile int64_t *seq = host_stats + CBTM_STAT_SEQ;
+    if (*seq >= frame) return 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned spins = 0;; ++spins) {
+        if (*seq >= frame) break;
+        if ((spins & 1023u) == 1023u &&
+            (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count() >
+                timeout_ns)
+            return CBTM_E_TIMEOUT;
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return 0;
 }
 
 int cbtm_run_lod_sequence(const cbtm_pool *pool, const double *root_tris, const double *prm_host,

@@ -49,24 +49,32 @@ __device__ __forceinline__ unsigned long long global_ns()
 __device__ __forceinline__ void publish_frame(const ReducePublish &pub, uint32_t live_after, int tid)
 {
     if (!pub.ctl_stats) return;
-    if (tid < CBTM_STATS_WORDS) {
+    if (tid < CBTM_STATS_WORDS) { // one warp
         int64_t v = pub.ctl_stats[tid];
         if (tid == CBTM_STAT_LIVE_AFTER) v = live_after;
         if (tid == CBTM_STAT_FRAME) {
             v += 1;
             pub.ctl_stats[tid] = v;
         }
+        const int64_t frame = __shfl_sync(FULL_MASK, v, CBTM_STAT_FRAME);
+        if (tid == CBTM_STAT_SEQ) v = frame;
         if (tid >= CBTM_STAT_PHASE_NS && tid < CBTM_STAT_PHASE_NS + CBTM_STAT_PHASES) {
             v = 0;
-            if (pub.phase_t) { // stamp k = start of phase k; the reduction ends now
+            if (pub.phase_t) { // stamp k = start of phase k; the frame ends now
                 const int k = tid - CBTM_STAT_PHASE_NS;
                 const unsigned long long t0 = pub.phase_t[k];
                 const unsigned long long t1 = k + 1 < CBTM_STAT_PHASES ? pub.phase_t[k + 1] : global_ns();
                 v = t1 > t0 ? (int64_t)(t1 - t0) : 0;
             }
         }
-        if (pub.pool_stats) pub.pool_stats[tid] = v;
         if (pub.stats_seq) pub.stats_seq[(size_t)CBTM_STATS_WORDS * (*pub.seq_frame) + tid] = v;
+        // pool stats may live in host-mapped memory: counters first, fence, sequence word last
+        if (pub.pool_stats) { // warp-uniform
+            if (tid != CBTM_STAT_SEQ) pub.pool_stats[tid] = v;
+            __threadfence_system();
+            __syncwarp();
+            if (tid == CBTM_STAT_SEQ) *(volatile int64_t *)&pub.pool_stats[tid] = v;
+        }
         // the per-frame counters start the next frame at zero
         if (tid < CBTM_STAT_PHASE_NS && tid != CBTM_STAT_FRAME) pub.ctl_stats[tid] = 0;
     }

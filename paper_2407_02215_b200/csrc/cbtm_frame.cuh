@@ -1330,8 +1330,10 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         upper_reduce_phase(p.bits, a.ws.dirty, p.counters, g.lc, wroot, bid, nb);
         grid.sync();
         // the frame's counters go out while the next frame's index phase is already running
+        // (pool->stats may be host-mapped memory: only the launch's last frame pays for that write)
         if (bid == nb - 1) {
-            const ReducePublish pub = {ctl->stats, p.stats, stats_seq, &ctl->seq_frame, ctl->phase_t[f & 1]};
+            const ReducePublish pub = {ctl->stats, f == n_frames - 1 ? p.stats : nullptr, stats_seq, &ctl->seq_frame,
+                                       ctl->phase_t[f & 1]};
             publish_frame(pub, p.counters[1], threadIdx.x);
         }
     }

@@ -63,25 +63,23 @@ class UpdateStats:
 
     @classmethod
     def from_device_words(cls, words, epoch: int, times=None) -> "UpdateStats":
-        w = [int(x) for x in words]
-        np_ = len(_lib.PHASE_NAMES)
-        if times is None and len(w) >= _lib.STAT_PHASE_NS + np_ and any(w[_lib.STAT_PHASE_NS:_lib.STAT_PHASE_NS + np_]):
+        w = words if type(words) is list else [int(x) for x in words]
+        lo = _lib.STAT_PHASE_NS
+        ph = w[lo:lo + _N_PHASES]
+        if times is None and any(ph):
             # device-measured phase times (ns) folded onto the reference's nine stages:
             # t2 cache pointers = index (also resets the commands, stage 3); t4 generate commands =
             # classify + admission + scatter; t5 reserve = agreement + slot hand-out;
             # t6 = fused fill/neighbours/bitfield; t9 = reduction (+ stats publish)
-            ph = w[_lib.STAT_PHASE_NS:_lib.STAT_PHASE_NS + np_]
-            us = lambda *ks: sum(ph[k] for k in ks) // 1000  # noqa: E731
-            times = [0, us(0), 0, us(1), us(2, 3), us(4), 0, 0, us(5)]
-            phase_ns = list(ph)
+            times = [0, ph[0] // 1000, 0, ph[1] // 1000, (ph[2] + ph[3]) // 1000, ph[4] // 1000,
+                     0, 0, ph[5] // 1000]
         else:
-            phase_ns = [0] * np_
-        return cls(phase_ns=phase_ns, epoch=epoch, live_before=w[6], live_after=w[7],
-                   splits_applied=w[2], merges_applied=w[3],
-                   splits_rejected_oom=w[0], merges_rejected_oom=w[1],
-                   split_allocs=w[4], merge_allocs=w[5],
-                   stage_times_us=list(times) if times is not None else [0] * 9,
-                   reserved_slots=w[8], poison=w[10])
+            ph = [0] * _N_PHASES
+            times = list(times) if times is not None else [0] * 9
+        return cls(epoch, w[6], w[7], w[2], w[3], w[0], w[1], w[4], w[5], times, w[8], w[10], ph)
+
+
+_N_PHASES = len(_lib.PHASE_NAMES)
 
 
 def write_stats_csv(stats_list, no_timing: bool = False) -> str:
@@ -157,11 +155,20 @@ class UniformSplit(KernelDecide):
 
 
 def lod_verdict(state, prm) -> "_lib.CVerdict":
-    cv = _lib.CVerdict()
-    cv.mode = _lib.VERDICT_LOD
-    cv.root_tris = _lib.ptr(state.d_root_tris)
-    prm = np.ascontiguousarray(prm, dtype=np.float64)
-    C.memmove(cv.prm, prm.ctypes.data, 8 * _lib.PRM_WORDS)
+    cv = getattr(state, "_lod_cv", None)
+    if cv is None:
+        cv = _lib.CVerdict()
+        cv.mode = _lib.VERDICT_LOD
+        cv.root_tris = _lib.ptr(state.d_root_tris)
+        try:
+            state._lod_cv = cv  # one struct per state; prm is copied by value at every launch
+        except AttributeError:
+            pass
+    if isinstance(prm, C.Array):  # LodDecide._prm_c: a ctypes view of the packed parameters
+        C.memmove(cv.prm, prm, 8 * _lib.PRM_WORDS)
+    else:
+        prm = np.ascontiguousarray(prm, dtype=np.float64)
+        C.memmove(cv.prm, prm.ctypes.data, 8 * _lib.PRM_WORDS)
     return cv
 
 
@@ -219,14 +226,16 @@ class ParallelEngine:
         return verdicts
 
     def update(self, state: TriangulationState, decide, epoch: int = 0) -> UpdateStats:
-        """One full nine-stage update; returns its counters (one 128-byte
-        device->host read, which is also the only synchronisation)."""
+        """One full nine-stage update; returns its counters.  The frame kernel
+        writes them into host-mapped memory; waiting for their sequence word is
+        the only synchronisation (no copy, no stream synchronise)."""
         L = _lib.load()
-        t = _lib.torch()
         pool = state.c_pool()
         stream = state.stream()
+        seq_before = int(state._stats_np[_lib.STAT_SEQ])
         events = None
         if self.profile:
+            t = _lib.torch()
             events = [t.cuda.Event(enable_timing=True) for _ in range(3)]
             events[0].record()
         cv = decide.device_verdict(state) if isinstance(decide, KernelDecide) else None
@@ -250,8 +259,13 @@ class ParallelEngine:
                        "cbtm_update_finish")
             if events:
                 events[2].record()
-        state._pinned_stats.copy_(state.d_stats, non_blocking=True)
-        state.synchronize()
+        rc = L.cbtm_wait_frame(state._stats_host_ptr, seq_before + 1, 20_000_000_000)
+        if rc:
+            state.synchronize()  # surfaces a CUDA error if the frame kernel died
+            _lib.check(rc, "cbtm_wait_frame")
+        words = state._stats_np.tolist()
+        if keep_alive is not None or events:
+            state.synchronize()
         del keep_alive
         state._touched()
         times = None
@@ -259,7 +273,7 @@ class ParallelEngine:
             times = [0] * 9
             times[1] = int(events[0].elapsed_time(events[1]) * 1000)
             times[3] = int(events[1].elapsed_time(events[2]) * 1000)
-        stats = UpdateStats.from_device_words(state._pinned_stats.tolist(), epoch, times)
+        stats = UpdateStats.from_device_words(words, epoch, times)
         assert stats.live_after == (stats.live_before - stats.splits_applied
                                     + stats.split_allocs - stats.merges_applied
                                     + stats.merge_allocs), \

@@ -81,7 +81,12 @@ class TriangulationState:
         self.d_counter = t.zeros(1, dtype=t.int64, device=dev)
         self.d_bits = t.zeros(L.cbtm_bitfield_words(depth), dtype=t.int64, device=dev)
         self.d_counters = t.zeros(L.cbtm_counter_words(depth), dtype=t.int32, device=dev)
-        self.d_stats = t.zeros(_lib.STATS_WORDS, dtype=t.int64, device=dev)
+        # frame counters: pinned host memory mapped into the device's address space -- the frame
+        # kernel writes them straight to the host (sequence word last), ParallelEngine.update polls
+        # that word instead of copying the stats back and synchronising the stream
+        self.d_stats = t.zeros(_lib.STATS_WORDS, dtype=t.int64).pin_memory()
+        self._stats_np = self.d_stats.numpy()
+        self._stats_host_ptr = int(self.d_stats.data_ptr())
         self.d_dispatch = t.zeros(4, dtype=t.int32, device=dev)
         self.d_workspace = t.zeros(L.cbtm_workspace_bytes(depth), dtype=t.uint8, device=dev)
         # mesh operators used by the classifier (uploaded once)
@@ -100,7 +105,6 @@ class TriangulationState:
                        _scratch=self.d_workspace)
         self._version = 0
         self._snap: dict[str, tuple[int, np.ndarray]] = {}
-        self._pinned_stats = t.zeros(_lib.STATS_WORDS, dtype=t.int64).pin_memory()
 
     # -- C-ABI view -----------------------------------------------------------
     def stream(self) -> int:
@@ -238,8 +242,7 @@ class TriangulationState:
                                    exact_free_cache=self.exact_free_cache,
                                    staged_launches=self.staged_launches)
         for k in ("ids", "nexts", "prevs", "twins", "commands", "reserved",
-                  "cache_live", "cache_free", "counter", "bits", "counters",
-                  "stats"):
+                  "cache_live", "cache_free", "counter", "bits", "counters"):
             getattr(other, "d_" + k).copy_(getattr(self, "d_" + k))
         other.max_depth = self.max_depth
         other._touched()
