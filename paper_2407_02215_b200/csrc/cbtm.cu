@@ -143,9 +143,13 @@ int index_launch(const cbtm_pool *pool, bool reset_commands, cudaStream_t st)
     const Geo g = make_geo(pool->depth);
     int32_t *freep = (pool->flags & CBTM_POOL_FULL_FREE_CACHE) ? pool->cache_free : nullptr;
     const unsigned grid = strided_grid(g.nblocks, IDX_WARPS, 6);
-    k_index<<<grid, IDX_WARPS * 32, 0, st>>>(reinterpret_cast<const uint32_t *>(pool->bits),
-                                             pool->counters, pool->depth, pool->cache_live, freep,
-                                             pool->dispatch, reset_commands ? pool->commands : nullptr);
+    if (reset_commands)
+        k_index<true><<<grid, IDX_WARPS * 32, 0, st>>>(reinterpret_cast<const uint32_t *>(pool->bits), pool->counters,
+                                                       pool->depth, pool->cache_live, freep, pool->dispatch,
+                                                       pool->commands);
+    else
+        k_index<false><<<grid, IDX_WARPS * 32, 0, st>>>(reinterpret_cast<const uint32_t *>(pool->bits), pool->counters,
+                                                        pool->depth, pool->cache_live, freep, pool->dispatch, nullptr);
     return launch_status();
 }
 
@@ -269,7 +273,7 @@ int cbtm_index(const uint64_t *bits, const uint32_t *counters, int depth, int32_
     if (!bits || !counters || !cache_live) return CBTM_E_NULL;
     if (((uintptr_t)bits | (uintptr_t)cache_live | (uintptr_t)cache_free) & 15) return CBTM_E_ALIGN;
     const Geo g = make_geo(depth);
-    k_index<<<strided_grid(g.nblocks, IDX_WARPS, 6), IDX_WARPS * 32, 0, as_stream(stream)>>>(
+    k_index<false><<<strided_grid(g.nblocks, IDX_WARPS, 6), IDX_WARPS * 32, 0, as_stream(stream)>>>(
         reinterpret_cast<const uint32_t *>(bits), counters, depth, cache_live, cache_free, dispatch, nullptr);
     return launch_status();
 }

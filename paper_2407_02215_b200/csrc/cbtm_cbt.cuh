@@ -530,6 +530,7 @@ __device__ __forceinline__ void fill_run_lines(int32_t *out, uint32_t first, uin
     }
 }
 
+template <bool RESET>
 __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32_t *counters, int depth,
                                             int32_t *cache_live, int32_t *cache_free, uint32_t *dispatch,
                                             uint32_t *reset_cmds, int32_t (*stage)[IDX_STAGE_WORDS],
@@ -576,7 +577,7 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
 
             if (cnt == 0 || cnt == g.span) { // uniform block: no expansion needed
                 fill_run_lines(cnt ? cache_live : cache_free, cnt ? ones_before : zeros_before, g.span, base, lane);
-                if (cnt && reset_cmds)
+                if (RESET && cnt)
                     for (uint32_t e = lane; e < g.span; e += 32) reset_cmds[(uint32_t)base + e] = 0u;
                 continue;
             }
@@ -598,7 +599,7 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
                     const int32_t slot = base + w * 32 + lane;
                     if ((word >> lane) & 1u) {
                         st[p1 + r1] = slot;
-                        if (reset_cmds) reset_cmds[slot] = 0u; // stage 3 (kernels.py:256-259)
+                        if (RESET) reset_cmds[slot] = 0u; // stage 3 (kernels.py:256-259)
                     } else if (want_free)
                         st[p0 + (uint32_t)lane - r1] = slot;
                     const uint32_t c = __popc(word);
@@ -617,7 +618,7 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
                     if ((uint32_t)lane < valid) {
                         if ((word >> lane) & 1u) {
                             st[p1 + r1] = slot;
-                            if (reset_cmds) reset_cmds[slot] = 0u;
+                            if (RESET) reset_cmds[slot] = 0u;
                         } else if (want_free)
                             st[p0 + (uint32_t)lane - r1] = slot;
                     }
@@ -635,13 +636,14 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
     }
 }
 
+template <bool RESET>
 __global__ void __launch_bounds__(IDX_WARPS * 32)
 k_index(const uint32_t *bits32, const uint32_t *counters, int depth, int32_t *cache_live,
         int32_t *cache_free, uint32_t *dispatch, uint32_t *reset_cmds)
 {
     __shared__ __align__(16) int32_t stage[IDX_WARPS][IDX_STAGE_WORDS];
-    index_phase(bits32, counters, depth, cache_live, cache_free, dispatch, reset_cmds, stage, blockIdx.x,
-                gridDim.x);
+    index_phase<RESET>(bits32, counters, depth, cache_live, cache_free, dispatch, reset_cmds, stage, blockIdx.x,
+                       gridDim.x);
 }
 
 // ---------------------------------------------------------------------------

@@ -1298,7 +1298,7 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         unsigned long long *stamp = stamper ? ctl->phase_t[f & 1] : nullptr;
         if (stamp) stamp[0] = global_ns();
         if (do_index)
-            index_phase(reinterpret_cast<const uint32_t *>(p.bits), p.counters, p.depth, p.cache_live,
+            index_phase<true>(reinterpret_cast<const uint32_t *>(p.bits), p.counters, p.depth, p.cache_live,
                         free_list, p.dispatch, p.commands,
                         reinterpret_cast<int32_t(*)[IDX_STAGE_WORDS]>(dyn_smem), bid, nb);
         else
