@@ -42,6 +42,7 @@ extern "C" {
 #define CBTM_LEAF_BLOCK_LOG2 10
 #define CBTM_STATS_WORDS 32
 #define CBTM_PRM_WORDS 23
+#define CBTM_MAX_BATCH 8 /* pools per cbtm_run_lod_sequence_batch call */
 
 /* contract violations */
 #define CBTM_E_DEPTH 1     /* depth outside [CBTM_MIN_DEPTH, CBTM_MAX_DEPTH] */
@@ -244,6 +245,17 @@ int cbtm_wait_frame(const int64_t *host_stats, int64_t frame, uint64_t timeout_n
 int cbtm_run_lod_sequence(const cbtm_pool *pool, const double *root_tris,
                           const double *prm_host, int32_t n_frames, int64_t *stats_out,
                           uintptr_t stream);
+
+/* ---- the same for a BATCH of independent pools (cmd_animate over several planets, BASELINE
+ *      config 5): the n_pools <= CBTM_MAX_BATCH pools advance in lockstep inside one cooperative
+ *      launch, sharing every grid barrier -- P latency-bound planets cost little more than one.
+ *      pools / root_tris / prm_host / stats_out are HOST arrays of n_pools entries: pool structs
+ *      (by value), device f64[H*9] pointers, host f64[n_frames*23] pointers and device
+ *      i64[n_frames*CBTM_STATS_WORDS] pointers (stats_out or any entry may be NULL).  Results are
+ *      identical to n_pools separate cbtm_run_lod_sequence calls.  n_frames <= 4096 per call. */
+int cbtm_run_lod_sequence_batch(const cbtm_pool *pools, int32_t n_pools, const double *const *root_tris,
+                                const double *const *prm_host, int32_t n_frames,
+                                int64_t *const *stats_out, uintptr_t stream);
 
 #ifdef __cplusplus
 }

@@ -24,6 +24,7 @@ STAT_SEQ = 31
 PHASE_NAMES = ("index", "classify_admit_scatter", "agree", "reserve", "apply", "reduce_publish")
 MIN_DEPTH = 1
 MAX_DEPTH_ABI = 30
+MAX_BATCH = 8
 
 POOL_FULL_FREE_CACHE = 1
 POOL_STAGED_LAUNCHES = 2
@@ -89,6 +90,7 @@ SIGNATURES = {
     "cbtm_update_finish": (C.c_int, [C.POINTER(CPool), C.POINTER(CVerdict), _UP]),
     "cbtm_run_lod_sequence": (C.c_int, [C.POINTER(CPool), _P, _P, C.c_int32, _P, _UP]),
     "cbtm_wait_frame": (C.c_int, [_P, _I64, C.c_uint64]),
+    "cbtm_run_lod_sequence_batch": (C.c_int, [C.POINTER(CPool), C.c_int32, _P, _P, C.c_int32, _P, _UP]),
 }
 
 _lib = None

@@ -53,20 +53,18 @@ def run_planet_batch(sequences, frames_params, world: int = 1, rank: int = 0,
                      device=None):
     """Advance this rank's planets frame by frame (GPU).  ``sequences`` are
     workloads.LodSequence objects, ``frames_params[p]`` is float64[frames, 23].
-    Planets of one rank are interleaved frame by frame on the same stream (each
-    frame is a fixed chain of launches), which keeps the GPU fed while any one
-    planet's chain is latency bound.  Returns (states, int64[owned, frames, STATS_WORDS])."""
+    The planets of one rank advance in lockstep inside one cooperative launch
+    (``pipeline.run_lod_sequence_batch``): a single planet's frame is latency
+    bound and leaves the GPU mostly idle, a batch shares every grid barrier and
+    round trip.  Returns (states, int64[owned, frames, STATS_WORDS])."""
     from . import _lib
-    from .pipeline import ParallelEngine
+    from .pipeline import run_lod_sequence_batch
     from .state import initialize
 
     owned = planets_of_rank(len(sequences), world, rank)
-    eng = ParallelEngine()
     states = [initialize(sequences[p].mesh, sequences[p].depth, device=device) for p in owned]
-    rows = []
-    for k, p in enumerate(owned):
-        stats = eng.run_lod_sequence(states[k], frames_params[p])
-        rows.append([[s.splits_rejected_oom, s.merges_rejected_oom, s.splits_applied,
-                      s.merges_applied, s.split_allocs, s.merge_allocs, s.live_before,
-                      s.live_after] + [0] * (_lib.STATS_WORDS - 8) for s in stats])
+    per_planet = run_lod_sequence_batch(states, [frames_params[p] for p in owned])
+    rows = [[[s.splits_rejected_oom, s.merges_rejected_oom, s.splits_applied,
+              s.merges_applied, s.split_allocs, s.merge_allocs, s.live_before,
+              s.live_after] + [0] * (_lib.STATS_WORDS - 8) for s in stats] for stats in per_planet]
     return states, np.array(rows, dtype=np.int64).reshape(len(owned), -1, _lib.STATS_WORDS)

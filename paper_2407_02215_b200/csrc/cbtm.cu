@@ -460,4 +460,71 @@ int cbtm_run_lod_sequence(const cbtm_pool *pool, const double *root_tris, const 
     return 0;
 }
 
+int cbtm_run_lod_sequence_batch(const cbtm_pool *pools, int32_t n_pools, const double *const *root_tris,
+                                const double *const *prm_host, int32_t n_frames, int64_t *const *stats_out,
+                                uintptr_t stream)
+{
+    if (!pools || !root_tris || !prm_host) return CBTM_E_NULL;
+    if (n_pools < 1 || n_pools > CBTM_MAX_BATCH || n_frames < 0 || n_frames > MAX_SEQ_FRAMES) return CBTM_E_RANGE;
+    cudaStream_t st = as_stream(stream);
+    BatchArgs b; // passed by value
+    int max_depth = 0;
+    bool any_staged = false;
+    for (int q = 0; q < n_pools; ++q) {
+        int rc = check_pool(&pools[q], true);
+        if (rc) return rc;
+        if (!root_tris[q] || !prm_host[q]) return CBTM_E_NULL;
+        for (int r = 0; r < q; ++r)
+            if (pools[r].workspace == pools[q].workspace || pools[r].bits == pools[q].bits) return CBTM_E_RANGE;
+        cbtm_verdict v;
+        v.mode = CBTM_VERDICT_LOD;
+        v.value = 0;
+        v.explicit_verdicts = nullptr;
+        v.root_tris = root_tris[q];
+        for (int k = 0; k < CBTM_PRM_WORDS; ++k) v.prm[k] = 0.0;
+        rc = fill_args(&pools[q], &v, &b.a[q]);
+        if (rc) return rc;
+        b.a[q].use_prm_seq = 1;
+        b.stats_seq[q] = stats_out ? stats_out[q] : nullptr;
+        if (pools[q].depth > max_depth) max_depth = pools[q].depth;
+        any_staged |= staged(&pools[q]);
+    }
+    if (n_frames == 0) return 0;
+    static int batch_per_sm = -1; // co-resident CTAs per SM of the batch kernel (0: no cooperative launch)
+    if (batch_per_sm < 0) {
+        int per_sm = 0;
+        batch_per_sm = 0;
+        if (persistent_grid(max_depth) != 0 &&
+            cudaFuncSetAttribute(k_frames_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, FRAMES_DYN_SMEM) ==
+                cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_frames_batch, CHUNK, FRAMES_DYN_SMEM) ==
+                cudaSuccess)
+            batch_per_sm = per_sm > BATCH_CTAS_PER_SM ? BATCH_CTAS_PER_SM : per_sm;
+        (void)cudaGetLastError();
+    }
+    const int batch_ok = batch_per_sm > 0;
+    if (!batch_ok || any_staged || n_pools == 1) { // one pool after the other (same results)
+        for (int q = 0; q < n_pools; ++q) {
+            const int rc = cbtm_run_lod_sequence(&pools[q], root_tris[q], prm_host[q], n_frames,
+                                                 stats_out ? stats_out[q] : nullptr, stream);
+            if (rc) return rc;
+        }
+        return 0;
+    }
+    for (int q = 0; q < n_pools; ++q) {
+        int rc = status(cudaMemcpyAsync(b.a[q].ws.prm_seq, prm_host[q], sizeof(double) * CBTM_PRM_WORDS * n_frames,
+                                        cudaMemcpyHostToDevice, st));
+        if (rc) return rc;
+        rc = status(cudaMemsetAsync(&b.a[q].ws.ctl->seq_frame, 0, sizeof(uint32_t), st));
+        if (rc) return rc;
+    }
+    uint64_t want = 0; // chunks of all pools if every slot were live: tiny pools get a small grid
+    for (int q = 0; q < n_pools; ++q) want += (((uint64_t)1 << pools[q].depth) + CHUNK - 1) / CHUNK;
+    const uint64_t cap = (uint64_t)sm_count() * batch_per_sm;
+    const unsigned grid = (unsigned)(want < cap ? want : cap);
+    void *args[] = {(void *)&b, (void *)&n_pools, (void *)&n_frames};
+    return status(cudaLaunchCooperativeKernel((const void *)k_frames_batch, dim3(grid), dim3(CHUNK), args,
+                                              FRAMES_DYN_SMEM, st));
+}
+
 } // extern "C"

@@ -492,27 +492,36 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t bid,
         __syncthreads();
     }
 
-    if (fast && bid == nb - 1) {
-        // admin: T = total need once every chunk has reported; then the window table
-        __shared__ unsigned long long s_total;
-        if (tid == 0) {
-            unsigned long long v;
-            do asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&ctl->need_total) : "memory");
-            while ((v >> NEED_TOTAL_SHIFT) < (unsigned long long)nch * (CHUNK / 32));
-            const unsigned long long total = v & ((1ull << NEED_TOTAL_SHIFT) - 1);
-            s_total = total;
-            ctl->need_total = 0; // nobody adds any more this frame
-            ctl->n = n;
-            ctl->F = (int64_t)(((uint64_t)1 << p.depth) - n);
-            ctl->T = (int64_t)total;
-            ctl->i0 = n;
-            ctl->tail_count = 0;
-            ctl->stats[CBTM_STAT_LIVE_BEFORE] = n;
-            ctl->stats[CBTM_STAT_RESERVED] = (int64_t)total;
-        }
-        __syncthreads();
-        build_window_table(a, (long long)s_total);
+}
+
+// Fast path, admin CTA: T = total need once every chunk has reported (waits for
+// the other CTAs' chunks, so a CTA with chunks of several pools calls it only
+// after all of them), then the window table.
+__device__ __forceinline__ void phase_classify_admin(const FrameArgs &a)
+{
+    __shared__ unsigned long long s_total;
+    const cbtm_pool &p = a.pool;
+    Control *ctl = a.ws.ctl;
+    const uint32_t n = p.counters[1];
+    if (!fits_a_priori(p, n)) return;
+    const uint32_t nch = (n + CHUNK - 1) / CHUNK;
+    if (threadIdx.x == 0) {
+        unsigned long long v;
+        do asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&ctl->need_total) : "memory");
+        while ((v >> NEED_TOTAL_SHIFT) < (unsigned long long)nch * (CHUNK / 32));
+        const unsigned long long total = v & ((1ull << NEED_TOTAL_SHIFT) - 1);
+        s_total = total;
+        ctl->need_total = 0; // nobody adds any more this frame
+        ctl->n = n;
+        ctl->F = (int64_t)(((uint64_t)1 << p.depth) - n);
+        ctl->T = (int64_t)total;
+        ctl->i0 = n;
+        ctl->tail_count = 0;
+        ctl->stats[CBTM_STAT_LIVE_BEFORE] = n;
+        ctl->stats[CBTM_STAT_RESERVED] = (int64_t)total;
     }
+    __syncthreads();
+    build_window_table(a, (long long)s_total);
 }
 
 // ---------------------------------------------------------------------------
@@ -1241,6 +1250,7 @@ __global__ void __launch_bounds__(CHUNK) k_reset(const __grid_constant__ FrameAr
 __global__ void __launch_bounds__(CHUNK) k_classify_frame(const __grid_constant__ FrameArgs a)
 {
     phase_classify(a, blockIdx.x, gridDim.x);
+    if (blockIdx.x == gridDim.x - 1) phase_classify_admin(a);
 }
 
 __global__ void __launch_bounds__(CHUNK) k_admit(const __grid_constant__ FrameArgs a)
@@ -1307,6 +1317,7 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         if (stamp) stamp[1] = global_ns();
         const bool fast = fits_a_priori(p, p.counters[1]); // grid-uniform
         phase_classify(a, bid, nb);
+        if (bid == nb - 1) phase_classify_admin(a);
         grid.sync();
         if (!fast) { // pool under reservation pressure: one CTA admits, then everybody scatters
             if (bid == 0) phase_admit<CHUNK>(a);
@@ -1336,6 +1347,113 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
                                        ctl->phase_t[f & 1]};
             publish_frame(pub, p.counters[1], threadIdx.x);
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Batches of independent pools (BASELINE config 5: several planets per GPU).
+// A frame of one planet leaves the GPU mostly idle (latency bound, a few hundred
+// CTAs' worth of work), so the planets of a batch advance in lockstep inside ONE
+// cooperative launch: every phase runs over all pools before the grid barrier
+// that ends it -- P planets pay for the barriers and the dependent round trips
+// of one.  Pool q sees the CTAs rotated by q * nb / P, which spreads the chunks
+// (and the admin / single-CTA duties) of the pools over different SMs.
+// ---------------------------------------------------------------------------
+constexpr int BATCH_CTAS_PER_SM = 4; // more chunks in flight per SM: a batch has work for them
+
+struct BatchArgs {
+    FrameArgs a[CBTM_MAX_BATCH];
+    int64_t *stats_seq[CBTM_MAX_BATCH];
+};
+
+__global__ void __launch_bounds__(CHUNK, BATCH_CTAS_PER_SM)
+k_frames_batch(const __grid_constant__ BatchArgs b, int n_pools, int n_frames)
+{
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(128) uint8_t dyn_smem[];
+    __shared__ uint32_t wroot[2][RED_THREADS / 32];
+
+    const uint32_t bid = blockIdx.x, nb = gridDim.x;
+    const uint32_t shift = nb / (uint32_t)n_pools;
+    auto vbid = [&](int q) { return (bid + (uint32_t)q * shift) % nb; };
+    auto stamp = [&](int f, int k) { // every pool records the batch's phase boundaries
+        if (bid == 0 && threadIdx.x == 0) {
+            const unsigned long long t = global_ns();
+            for (int q = 0; q < n_pools; ++q) b.a[q].ws.ctl->phase_t[f & 1][k] = t;
+        }
+    };
+
+    for (int f = 0; f < n_frames; ++f) {
+        stamp(f, 0);
+        for (int q = 0; q < n_pools; ++q) {
+            const FrameArgs &a = b.a[q];
+            const cbtm_pool &p = a.pool;
+            index_phase<true>(reinterpret_cast<const uint32_t *>(p.bits), p.counters, p.depth, p.cache_live,
+                              (p.flags & CBTM_POOL_FULL_FREE_CACHE) ? p.cache_free : nullptr, p.dispatch, p.commands,
+                              reinterpret_cast<int32_t(*)[IDX_STAGE_WORDS]>(dyn_smem), vbid(q), nb);
+            __syncthreads(); // the staging area is reused by the next pool
+        }
+        grid.sync();
+        stamp(f, 1);
+        bool any_slow = false; // grid-uniform
+        for (int q = 0; q < n_pools; ++q) {
+            any_slow |= !fits_a_priori(b.a[q].pool, b.a[q].pool.counters[1]);
+            phase_classify(b.a[q], vbid(q), nb);
+            __syncthreads();
+        }
+        for (int q = 0; q < n_pools; ++q) // admin duties last: they wait for the other CTAs' chunks
+            if (vbid(q) == nb - 1) {
+                phase_classify_admin(b.a[q]);
+                __syncthreads();
+            }
+        grid.sync();
+        if (any_slow) { // pools under reservation pressure: one CTA each admits, then everybody scatters
+            for (int q = 0; q < n_pools; ++q)
+                if (vbid(q) == 0 && !fits_a_priori(b.a[q].pool, b.a[q].pool.counters[1])) phase_admit<CHUNK>(b.a[q]);
+            grid.sync();
+            for (int q = 0; q < n_pools; ++q)
+                if (!fits_a_priori(b.a[q].pool, (uint32_t)b.a[q].ws.ctl->n)) {
+                    phase_scatter(b.a[q], vbid(q), nb);
+                    __syncthreads();
+                }
+            grid.sync();
+        }
+        stamp(f, 2);
+        for (int q = 0; q < n_pools; ++q) {
+            phase_agree(b.a[q], vbid(q), nb);
+            __syncthreads();
+        }
+        grid.sync();
+        stamp(f, 3);
+        for (int q = 0; q < n_pools; ++q) {
+            phase_reserve(b.a[q], vbid(q), nb);
+            __syncthreads();
+        }
+        grid.sync();
+        stamp(f, 4);
+        for (int q = 0; q < n_pools; ++q) {
+            phase_apply(b.a[q], vbid(q), nb);
+            __syncthreads();
+        }
+        grid.sync();
+        stamp(f, 5);
+        if (bid == 0 && threadIdx.x == 0) __threadfence();
+        for (int q = 0; q < n_pools; ++q) {
+            const cbtm_pool &p = b.a[q].pool;
+            upper_reduce_phase(p.bits, b.a[q].ws.dirty, p.counters, make_geo(p.depth).lc, wroot, vbid(q), nb);
+            __syncthreads();
+        }
+        grid.sync();
+        for (int q = 0; q < n_pools; ++q)
+            if (vbid(q) == nb - 1) {
+                const FrameArgs &a = b.a[q];
+                Control *ctl = a.ws.ctl;
+                const ReducePublish pub = {ctl->stats, f == n_frames - 1 ? a.pool.stats : nullptr, b.stats_seq[q],
+                                           &ctl->seq_frame, ctl->phase_t[f & 1]};
+                publish_frame(pub, a.pool.counters[1], threadIdx.x);
+                __syncthreads();
+            }
     }
 }
 

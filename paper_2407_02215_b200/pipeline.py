@@ -309,6 +309,50 @@ class ParallelEngine:
         return [UpdateStats.from_device_words(rows[f], first_epoch + f) for f in range(n)]
 
 
+def run_lod_sequence_batch(states, params_list, first_epoch: int = 0) -> list[list[UpdateStats]]:
+    """Camera sequences of several independent planets on one GPU, advanced in
+    lockstep inside one cooperative launch per group of up to ``_lib.MAX_BATCH``
+    states (cbtm_run_lod_sequence_batch; BASELINE config 5).  ``params_list[p]``
+    is float64[n_frames, 23] for ``states[p]``; all sequences have the same
+    length.  Results are identical to one ``run_lod_sequence`` per state."""
+    L = _lib.load()
+    t = _lib.torch()
+    if len(states) != len(params_list):
+        raise ValueError("one parameter array per state")
+    if not states:
+        return []
+    prm = [np.ascontiguousarray(p, dtype=np.float64).reshape(-1, _lib.PRM_WORDS) for p in params_list]
+    n = prm[0].shape[0]
+    if any(p.shape[0] != n for p in prm):
+        raise ValueError("all sequences of a batch must have the same number of frames")
+    device = states[0].device
+    if any(s.device != device for s in states):
+        raise ValueError("the states of a batch must live on one device")
+    out = []
+    for g0 in range(0, len(states), _lib.MAX_BATCH):
+        group = states[g0:g0 + _lib.MAX_BATCH]
+        k = len(group)
+        d_stats = [t.zeros((max(n, 1), _lib.STATS_WORDS), dtype=t.int64, device=device) for _ in group]
+        pools = (_lib.CPool * k)(*[s.c_pool() for s in group])
+        roots = (C.c_void_p * k)(*[_lib.ptr(s.d_root_tris) for s in group])
+        prms = (C.c_void_p * k)(*[p.ctypes.data for p in prm[g0:g0 + k]])
+        souts = (C.c_void_p * k)(*[_lib.ptr(d) for d in d_stats])
+        for done in range(0, max(n, 1), 4096):  # MAX_SEQ_FRAMES per launch
+            cnt = min(4096, n - done)
+            if cnt <= 0:
+                break
+            prms_d = (C.c_void_p * k)(*[p.ctypes.data + 8 * _lib.PRM_WORDS * done for p in prm[g0:g0 + k]])
+            souts_d = (C.c_void_p * k)(*[_lib.ptr(d) + 8 * _lib.STATS_WORDS * done for d in d_stats])
+            rc = L.cbtm_run_lod_sequence_batch(pools, k, roots, prms_d, cnt, souts_d, group[0].stream())
+            _lib.check(rc, "cbtm_run_lod_sequence_batch")
+        del prms, souts
+        for s, d in zip(group, d_stats):
+            rows = _lib.to_host(d)
+            s._touched()
+            out.append([UpdateStats.from_device_words(rows[f], first_epoch + f) for f in range(n)])
+    return out
+
+
 class EpochFactory:
     """Wraps an epoch-indexed family of decide functions for run_epochs."""
 

@@ -161,3 +161,29 @@ def test_sequence_runner_matches_per_frame_updates():
         if k != "cache_free":
             assert np.array_equal(ha[k], hb[k]), k
             assert np.array_equal(ha[k], hc[k]), k
+
+
+def test_batch_kernel_equals_separate_sequences():
+    """cbtm_run_lod_sequence_batch (several planets in lockstep inside one
+    cooperative launch, BASELINE config 5) == one sequence run per planet.
+    Mixed batch: pools of different depth and mesh, one of them small enough to
+    run under reservation pressure (admission tail path) next to pools on the
+    a-priori fast path."""
+    from paper_2407_02215_b200.pipeline import run_lod_sequence_batch
+    seqs = [workloads.cube_sphere_flyin(depth=18, frames=20),
+            workloads.earth_sweep(depth=20, frames=20, rotate_deg=45.0),
+            workloads.cube_sphere_flyin(depth=12, frames=20),      # tiny pool: constant OOM pressure
+            workloads.earth_sweep(depth=22, frames=20, rotate_deg=90.0),
+            workloads.earth_sweep(depth=16, frames=20)]
+    prms = [s.params()[:20] for s in seqs]
+    solo = [initialize(s.mesh, s.depth) for s in seqs]
+    both = [initialize(s.mesh, s.depth) for s in seqs]
+    with ParallelEngine() as eng:
+        want = [eng.run_lod_sequence(st, p) for st, p in zip(solo, prms)]
+    got = run_lod_sequence_batch(both, prms)
+    assert any(w.splits_rejected_oom + w.merges_rejected_oom for w in want[2]), "pressure case lost its pressure"
+    for p, (w, g) in enumerate(zip(want, got)):
+        assert [stats_words(s) for s in w] == [stats_words(s) for s in g], f"planet {p}: stats"
+        ha, hb = solo[p].to_host(), both[p].to_host()
+        for k in ha:
+            assert np.array_equal(ha[k], hb[k]), f"planet {p}: {k}"
