@@ -192,6 +192,26 @@ int cbtm_export_nodes(const uint64_t *bits, const uint32_t *counters, int depth,
 int cbtm_initialize(const cbtm_pool *pool, const int32_t *he_next, const int32_t *he_prev,
                     const int32_t *he_twin, int32_t n_halfedges, uintptr_t stream);
 
+/* ---- halfedge.from_polygons (halfedge.py:158-212) on the device, for input meshes too large for
+ *      the python dictionaries of the reference (the paper's 21 399-halfedge asset and beyond).
+ *      Input: polygon loops in CSR form, face_offsets i32[F+1] and face_verts i32[H] (device).
+ *      Output (device i32[H] each): the six halfedge operators twin / next / prev / vert / edge /
+ *      face exactly as the reference numbers them (halfedges in face order, edge = rank of the
+ *      undirected vertex pair in sorted order, twin = -1 on a boundary).  status (device
+ *      i64[CBTM_MESH_STATUS_WORDS]) = {degenerate faces (< 3 distinct vertices), corners with a
+ *      vertex outside [0, V), zero-length edges, non-manifold edges (> 2 halfedges), edges whose
+ *      two halfedges share a direction (inconsistent winding), lowest offending face or -1,
+ *      lowest offending edge key (min << 32 | max) or -1, number of edges}: a mesh is valid iff
+ *      the first five words are 0 -- the conditions under which the reference raises MeshError.
+ *      workspace: cbtm_mesh_workspace_bytes(H) bytes of device scratch. */
+#define CBTM_MESH_STATUS_WORDS 8
+size_t cbtm_mesh_workspace_bytes(int64_t n_halfedges);
+int cbtm_mesh_from_polygons(const int32_t *face_offsets, const int32_t *face_verts, int32_t n_faces,
+                            int32_t n_halfedges, int32_t n_vertices, int32_t *he_twin,
+                            int32_t *he_next, int32_t *he_prev, int32_t *he_vert, int32_t *he_edge,
+                            int32_t *he_face, int64_t *status, void *workspace,
+                            size_t workspace_bytes, uintptr_t stream);
+
 /* ---- root bisector vertices per halfedge (bisector.py:154-173): v0, v1 and
  *      the face mean accumulated along `next`; out f64[H*9]. */
 int cbtm_root_triangles(const int32_t *he_next, const int32_t *he_vert,

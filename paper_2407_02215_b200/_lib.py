@@ -81,6 +81,8 @@ SIGNATURES = {
     "cbtm_import_leaves": (C.c_int, [_P, _I, _P, _UP]),
     "cbtm_export_nodes": (C.c_int, [_P, _P, _I, _P, _UP]),
     "cbtm_initialize": (C.c_int, [C.POINTER(CPool), _P, _P, _P, C.c_int32, _UP]),
+    "cbtm_mesh_workspace_bytes": (_SZ, [_I64]),
+    "cbtm_mesh_from_polygons": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _UP]),
     "cbtm_root_triangles": (C.c_int, [_P, _P, _P, C.c_int32, _P, _UP]),
     "cbtm_classify": (C.c_int, [C.POINTER(CPool), C.POINTER(CVerdict), _P, _UP]),
     "cbtm_decode_triangles": (C.c_int, [_P, _I64, C.c_int32, _P, _P, _UP]),

@@ -12,7 +12,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcbtm.so")
 SOURCES = ["cbtm.cu"]
 HEADERS = ["cbtm_common.cuh", "cbtm_cbt.cuh", "cbtm_classify.cuh",
-           "cbtm_frame.cuh", os.path.join("..", "..", "include", "cbtm.h")]
+           "cbtm_frame.cuh", "cbtm_mesh.cuh", os.path.join("..", "..", "include", "cbtm.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

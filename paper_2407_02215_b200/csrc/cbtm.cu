@@ -8,6 +8,7 @@
 #include <chrono>
 
 #include "cbtm_frame.cuh"
+#include "cbtm_mesh.cuh"
 
 using namespace cbtm;
 
@@ -398,6 +399,51 @@ int cbtm_update(const cbtm_pool *pool, const cbtm_verdict *verdict, uintptr_t st
         return rc ? rc : finish_staged(a, nullptr, false, as_stream(stream));
     }
     return frames_launch(a, 1, nullptr, 1, grid, as_stream(stream));
+}
+
+size_t cbtm_mesh_workspace_bytes(int64_t n_halfedges)
+{
+    if (n_halfedges < 1 || n_halfedges > 0x7fffffff) return 0;
+    return carve_mesh_scratch(nullptr, n_halfedges, nullptr);
+}
+
+int cbtm_mesh_from_polygons(const int32_t *face_offsets, const int32_t *face_verts, int32_t n_faces,
+                            int32_t n_halfedges, int32_t n_vertices, int32_t *he_twin, int32_t *he_next,
+                            int32_t *he_prev, int32_t *he_vert, int32_t *he_edge, int32_t *he_face,
+                            int64_t *status_out, void *workspace, size_t workspace_bytes, uintptr_t stream)
+{
+    if (!face_offsets || !face_verts || !he_twin || !he_next || !he_prev || !he_vert || !he_edge || !he_face ||
+        !status_out || !workspace)
+        return CBTM_E_NULL;
+    if (n_faces < 1 || n_halfedges < 1 || n_vertices < 1) return CBTM_E_RANGE;
+    if (workspace_bytes < carve_mesh_scratch(nullptr, n_halfedges, nullptr)) return CBTM_E_WORKSPACE;
+    cudaStream_t st = as_stream(stream);
+    MeshScratch m;
+    carve_mesh_scratch(workspace, n_halfedges, &m);
+    unsigned long long *d_status = reinterpret_cast<unsigned long long *>(status_out);
+    int rc = status(cudaMemsetAsync(status_out, 0, sizeof(int64_t) * CBTM_MESH_STATUS_WORDS, st));
+    if (rc) return rc;
+    rc = status(cudaMemsetAsync(status_out + MESH_FIRST_FACE, 0xff, 2 * sizeof(int64_t), st)); // atomicMin targets
+    if (rc) return rc;
+    k_mesh_faces<<<strided_grid((uint64_t)n_faces, 256, 8), 256, 0, st>>>(face_offsets, face_verts, n_faces, n_vertices,
+                                                                        he_next, he_prev, he_vert, he_face, m.keys_a,
+                                                                        m.vals_a, d_status);
+    rc = launch_status();
+    if (rc) return rc;
+    int vbits = 1;
+    while (vbits < 32 && ((int64_t)1 << vbits) < (int64_t)n_vertices) ++vbits;
+    size_t tmp = m.cub_bytes;
+    rc = status(cub::DeviceRadixSort::SortPairs(m.cub_tmp, tmp, m.keys_a, m.keys_b, m.vals_a, m.vals_b, n_halfedges, 0,
+                                                32 + vbits, st));
+    if (rc) return rc;
+    k_mesh_run_starts<<<strided_grid((uint64_t)n_halfedges, 256, 8), 256, 0, st>>>(m.keys_b, n_halfedges, m.starts);
+    tmp = m.cub_bytes;
+    rc = status(cub::DeviceScan::ExclusiveSum(m.cub_tmp, tmp, m.starts, m.ranks, n_halfedges, st));
+    if (rc) return rc;
+    k_mesh_twins<<<strided_grid((uint64_t)n_halfedges, 256, 8), 256, 0, st>>>(m.keys_b, m.vals_b, m.starts, m.ranks,
+                                                                            n_halfedges, he_vert, he_twin, he_edge,
+                                                                            d_status);
+    return launch_status();
 }
 
 int cbtm_wait_frame(const int64_t *host_stats, int64_t frame, uint64_t timeout_ns)
