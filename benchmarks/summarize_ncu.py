@@ -27,7 +27,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 def launches(path, first=None, last=None):
     lines = [l for l in open(path) if l.startswith('"')]
     rows = list(csv.DictReader(lines))
-    ours = [(r["Kernel Name"].split("(")[0].replace("cbtm::", ""), float(r["Metric Value"]))
+    ours = [(r["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "").replace("cbtm::", ""),
+             float(r["Metric Value"]))
             for r in rows if r["Metric Name"] == "gpu__time_duration.sum" and "cbtm::" in r["Kernel Name"]]
     frames, cur = [], None
     for name, ns in ours:
