@@ -1,22 +1,33 @@
-import sys, numpy as np
-import os; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import bench, torch, ctypes as C
+"""Work vs barrier wait per phase of the frame kernel.  Needs a library built with -DCBTM_DEBUG_TIMING
+(every CTA records when its work of a phase ends):
+    nvcc ... -DCBTM_DEBUG_TIMING -o paper_2407_02215_b200/libcbtm.so paper_2407_02215_b200/csrc/cbtm.cu
+"""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import ctypes as C
+import numpy as np
+import torch
+import bench
 from paper_2407_02215_b200 import _lib
 from paper_2407_02215_b200.pipeline import ParallelEngine
 from paper_2407_02215_b200.state import initialize
-seq, down, cycle = bench.sweep_params(26, 0.0)
+
+depth = int(sys.argv[1]) if len(sys.argv) > 1 else 26
+seq, down, cycle = bench.sweep_params(depth, 0.0)
 eng = ParallelEngine()
-state = initialize(seq.mesh, 26)
+state = initialize(seq.mesh, depth)
 eng.run_lod_sequence(state, down)
 eng.run_lod_sequence(state, bench.step_params(cycle, 0, 8))
 prm = bench.step_params(cycle, 8, 64)
 L = _lib.load()
 d_stats = torch.zeros((64, _lib.STATS_WORDS), dtype=torch.int64, device=state.device)
 pool = state.c_pool()
-rc = L.cbtm_run_lod_sequence(C.byref(pool), _lib.ptr(state.d_root_tris), prm.ctypes.data, 64, _lib.ptr(d_stats), state.stream())
+_lib.check(L.cbtm_run_lod_sequence(C.byref(pool), _lib.ptr(state.d_root_tris), prm.ctypes.data, 64,
+                                   _lib.ptr(d_stats), state.stream()), "seq")
 torch.cuda.synchronize()
 rows = d_stats.cpu().numpy()
-names = ["P2:classified(cta0)", "P2:last lookback", "P2:last scattered", "P2:admin total", "P2:admin descent", "P2:admin done", "P3:agreed", "P3:lookback", "P3:expanded", "P3:reserved"]
-print("phases us:", rows[:, 16:22].mean(axis=0) / 1e3)
-for k, nm in enumerate(names):
-    print(f"{nm:24s} mean {rows[:, 22 + k].mean() / 1e3:7.2f} us  max {rows[:, 22 + k].max() / 1e3:7.2f}")
+print(f"{'phase':26s} {'total us':>9s} {'latest work end us':>19s} {'barrier + skew us':>18s}")
+for k, name in enumerate(_lib.PHASE_NAMES):
+    tot, work = rows[:, 16 + k].mean() / 1e3, rows[:, 22 + k].mean() / 1e3
+    print(f"{name:26s} {tot:9.2f} {work:19.2f} {tot - work:18.2f}")
+print(f"{'frame':26s} {rows[:, 16:22].sum(axis=1).mean() / 1e3:9.2f}")

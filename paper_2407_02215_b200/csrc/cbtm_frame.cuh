@@ -50,6 +50,14 @@
 
 #include <cooperative_groups.h>
 
+// -DCBTM_DEBUG_TIMING: every CTA records when its work of a phase ends (stats words 22..27 = latest end of work
+// relative to the phase start, in ns), to tell work from barrier wait (benchmarks/phase_probe.py)
+#ifdef CBTM_DEBUG_TIMING
+#define WORK_END(ctl, k) do { if (threadIdx.x == 0) atomicMax(&(ctl)->work_end[k], global_ns()); } while (0)
+#else
+#define WORK_END(ctl, k) do { } while (0)
+#endif
+
 #include "cbtm_cbt.cuh"
 #include "cbtm_classify.cuh"
 
@@ -71,6 +79,9 @@ struct Control {
     uint32_t win_n;  // leaf blocks in the window table (0: table not built, descend)
     unsigned long long phase_t[2][CBTM_STAT_PHASES + 1]; // %globaltimer at the start of each phase, by frame parity
     int64_t stats[CBTM_STATS_WORDS];
+#ifdef CBTM_DEBUG_TIMING
+    unsigned long long work_end[CBTM_STAT_PHASES]; // latest end of a CTA's work in each phase (before the barrier)
+#endif
 };
 
 constexpr int NEED_TOTAL_SHIFT = 40; // sum of needs < 2^30 * 187 < 2^38; warps of the live ranks < 2^24 on the fast path
@@ -171,6 +182,35 @@ __device__ __forceinline__ MergeCfg merge_config(const cbtm_pool &p, uint64_t j1
         jo = p.ids[oth];
         j4 = odd ? p.nexts[oth] : p.prevs[oth];
     }
+    if ((js >> 1) != (j1 >> 1)) return c;
+    c.sib = sib;
+    c.id_sib = js;
+    if (oth < 0) {
+        c.kind = 1;
+        return c;
+    }
+    if (bit_length64(jo) != bit_length64(j1)) return c;
+    if (j4 < 0) return c;
+    const uint64_t j4id = p.ids[j4];
+    if ((j4id >> 1) != (jo >> 1)) return c;
+    c.kind = 2;
+    c.oth = oth;
+    c.j4 = j4;
+    c.id_oth = jo;
+    c.id_j4 = j4id;
+    return c;
+}
+
+// The same test on values gathered ahead of time (phase_classify issues these
+// loads before the classifier runs so that their latency hides behind it):
+// js = ids[sib], jo = ids[oth], j4 = next-or-prev[oth]; only ids[j4] is still
+// to be fetched, and only for a quad.
+__device__ __forceinline__ MergeCfg merge_config_gathered(const cbtm_pool &p, uint64_t j1, int32_t sib, int32_t oth,
+                                                          uint64_t js, uint64_t jo, int32_t j4)
+{
+    MergeCfg c = {0, -1, -1, -1, 0, 0, 0};
+    if (depth_of(j1, p.rank) < 1) return c; // roots never merge
+    if (sib < 0) return c;
     if ((js >> 1) != (j1 >> 1)) return c;
     c.sib = sib;
     c.id_sib = js;
@@ -437,14 +477,24 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t bid,
         if (i < n) {
             s = p.cache_live[i];
             const uint64_t id = p.ids[s];
-            // merge requests need these; fetched now so the latency hides behind the classifier
             const int32_t nx = p.nexts[s], pv = p.prevs[s];
+            // what a merge request will ask about its sibling and the opposite pair: gathered now,
+            // for everybody, so that the round trip hides behind the classifier
+            const bool odd = id & 1;
+            const int32_t sib = odd ? pv : nx, oth = odd ? nx : pv;
+            uint64_t js = 0, jo = 0;
+            int32_t j4 = -1;
+            if (sib >= 0) js = p.ids[sib];
+            if (oth >= 0) {
+                jo = p.ids[oth];
+                j4 = odd ? p.nexts[oth] : p.prevs[oth];
+            }
             const int v = verdict_of(a, prm, id, i);
             if (v == 1) {
                 const int d = depth_of(id, p.rank);
                 if (d < p.max_depth) need = 3 * d + 4;
             } else if (v == 2) {
-                const MergeCfg c = merge_config(p, id, nx, pv);
+                const MergeCfg c = merge_config_gathered(p, id, sib, oth, js, jo, j4);
                 if (c.kind) {
                     need = 2;
                     mbits = CBTM_CMD_MERGE;
@@ -738,14 +788,17 @@ __device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t bid, ui
         uint32_t na = 0;
         if (i < n) {
             const int32_t s = p.cache_live[i];
+            const int32_t j4_hint = a.ws.j4s[i]; // meaningful only under a QUAD command of this frame
+            // the record's fields together with its command word: one round trip instead of two
             const uint32_t cmd = p.commands[s];
+            const uint64_t js = p.ids[s];
+            const int32_t nx = p.nexts[s], pv = p.prevs[s];
             const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
             int32_t ref = -1;
             if (sm) {
                 na = 2 + ((sm >> 1) & 1) + ((sm >> 2) & 1);
             } else if (cmd & CBTM_CMD_MERGE) {
-                const uint64_t js = p.ids[s];
-                const MergeCfg c = merge_config_admitted(js, p.nexts[s], p.prevs[s], cmd, a.ws.j4s[i]);
+                const MergeCfg c = merge_config_admitted(js, nx, pv, cmd, j4_hint);
                 // one round trip: the members' command words and ids
                 const uint32_t c_sib = p.commands[c.sib];
                 const uint64_t jb = p.ids[c.sib];
@@ -836,12 +889,15 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t bid, 
     long long off = 0;      // slots allocated by chunks [0, summed)
     uint32_t summed = 0;
     for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
+        // one round trip: the chunk's own count, this rank's count and slot, and the counts of the
+        // chunks between the previous chunk of this CTA and this one
         const uint32_t total = a.ws.chunk_alloc[chunk];
-        if (total == 0) continue; // CTA-uniform
-        off += (long long)cta_range_sum(a.ws.chunk_alloc, summed, chunk, scratch64);
-        summed = chunk;
         const uint32_t i = chunk * CHUNK + tid;
         const uint32_t na = i < n ? a.ws.nalloc8[i] : 0;
+        const int32_t s = i < n ? p.cache_live[i] : -1;
+        off += (long long)cta_range_sum(a.ws.chunk_alloc, summed, chunk, scratch64);
+        summed = chunk;
+        if (total == 0) continue; // CTA-uniform
         uint32_t total_chk;
         const uint32_t incl = block_inclusive_scan<CHUNK>(na, scratch, &total_chk);
 
@@ -884,7 +940,6 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t bid, 
             __syncthreads();
         }
         if (na) {
-            const int32_t s = p.cache_live[i];
             for (uint32_t k = 0; k < na; ++k) {
                 const long long r = base + k;
                 int32_t slot;
@@ -1092,12 +1147,30 @@ __device__ __forceinline__ void set_free(const BitSink &b, int32_t slot)
 }
 
 // kernels.py:373-461 restated over the two halves of the bisector
-__device__ __forceinline__ void apply_split(ApplyCtx &cx, int32_t s, uint32_t sm)
+// a consumed bisector's own record, fetched together with its command word
+struct OwnRecord {
+    uint64_t id;
+    int32_t nx, pv, tw;
+    int4 res;
+};
+
+__device__ __forceinline__ OwnRecord load_own(const cbtm_pool &p, int32_t s)
+{
+    OwnRecord r;
+    r.id = p.ids[s];
+    r.nx = p.nexts[s];
+    r.pv = p.prevs[s];
+    r.tw = p.twins[s];
+    r.res = *reinterpret_cast<const int4 *>(p.reserved + 4 * (size_t)s);
+    return r;
+}
+
+__device__ __forceinline__ void apply_split(ApplyCtx &cx, int32_t s, uint32_t sm, const OwnRecord &own)
 {
     const cbtm_pool &p = cx.p;
-    const uint64_t j = p.ids[s];
-    const int32_t nb_n = p.nexts[s], nb_p = p.prevs[s], nb_t = p.twins[s];
-    const int4 r4 = *reinterpret_cast<const int4 *>(p.reserved + 4 * (size_t)s);
+    const uint64_t j = own.id;
+    const int32_t nb_n = own.nx, nb_p = own.pv, nb_t = own.tw;
+    const int4 r4 = own.res;
     const Neighbour tn = load_neighbour(cx, nb_n), tp = load_neighbour(cx, nb_p), tt = load_neighbour(cx, nb_t);
     const bool split_p = sm & CBTM_CMD_SPLIT_P, split_n = sm & CBTM_CMD_SPLIT_N;
     const int left_n = split_p ? 2 : 1;
@@ -1184,35 +1257,41 @@ __device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t bid, ui
     for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
         const uint32_t i = chunk * CHUNK + tid;
         if (i >= n) continue;
-        if (a.ws.nalloc8[i] == 0) {
+        // round trip 1: by rank; round trip 2: everything about the own record at once
+        const uint32_t na = a.ws.nalloc8[i];
+        const int32_t s = p.cache_live[i];
+        const int32_t j4_hint = a.ws.j4s[i];
+        const uint32_t cmd = p.commands[s];
+        const int32_t mref = a.ws.merge_ref[s];
+        const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
+        if (na == 0) {
             // not allocating: either untouched, or a non-owner member of an agreed merge
-            const int32_t s = p.cache_live[i];
-            if (a.ws.merge_ref[s] >= 0 && !(p.commands[s] & CBTM_CMD_SPLIT_MASK)) {
+            if (!sm && mref >= 0) {
                 set_free(bits32, s);
                 ++merge_freed;
             }
             continue;
         }
-        const int32_t s = p.cache_live[i];
-        const uint32_t cmd = p.commands[s];
-        const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
+        const OwnRecord own = load_own(p, s);
         if (sm) {
-            apply_split(cx, s, sm);
+            apply_split(cx, s, sm, own);
             ++split_freed;
             split_alloc += 2 + ((sm >> 1) & 1) + ((sm >> 2) & 1);
         } else { // owner of an agreed merge: kernels.py:464-491, 562-594, 624-628
             set_free(bits32, s);
             ++merge_freed;
-            const uint64_t js = p.ids[s];
-            const MergeCfg c = merge_config_admitted(js, p.nexts[s], p.prevs[s], cmd, a.ws.j4s[i]);
+            const uint64_t js = own.id;
+            const MergeCfg c = merge_config_admitted(js, own.nx, own.pv, cmd, j4_hint);
             const bool s_even = !(js & 1);
-            const int32_t p1 = p.reserved[4 * (size_t)s];
-            const uint64_t id_e1 = s_even ? js : p.ids[c.sib];
+            const int32_t p1 = own.res.x;
+            const uint64_t id_sib = p.ids[c.sib];
+            const uint64_t id_e1 = s_even ? js : id_sib;
             if (c.kind == 2) {
-                const int32_t p2 = p.reserved[4 * (size_t)s + 1];
+                const int32_t p2 = own.res.y;
                 const uint64_t jo = p.ids[c.oth];
+                const uint64_t id_j4 = p.ids[c.j4];
                 const bool oth_even = !(jo & 1);
-                const uint64_t id_e2 = oth_even ? jo : p.ids[c.j4];
+                const uint64_t id_e2 = oth_even ? jo : id_j4;
                 apply_merged_pair(cx, s_even ? s : c.sib, s_even ? c.sib : s, id_e1, p1, p2);
                 apply_merged_pair(cx, oth_even ? c.oth : c.j4, oth_even ? c.j4 : c.oth, id_e2, p2, p1);
                 set_live(bits32, p1);
@@ -1313,11 +1392,13 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
                         reinterpret_cast<int32_t(*)[IDX_STAGE_WORDS]>(dyn_smem), bid, nb);
         else
             phase_reset(a, bid, nb);
+        WORK_END(ctl, 0);
         grid.sync();
         if (stamp) stamp[1] = global_ns();
         const bool fast = fits_a_priori(p, p.counters[1]); // grid-uniform
         phase_classify(a, bid, nb);
         if (bid == nb - 1) phase_classify_admin(a);
+        WORK_END(ctl, 1);
         grid.sync();
         if (!fast) { // pool under reservation pressure: one CTA admits, then everybody scatters
             if (bid == 0) phase_admit<CHUNK>(a);
@@ -1327,18 +1408,22 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         }
         if (stamp) stamp[2] = global_ns();
         phase_agree(a, bid, nb);
+        WORK_END(ctl, 2);
         grid.sync();
         if (stamp) stamp[3] = global_ns();
         phase_reserve(a, bid, nb);
+        WORK_END(ctl, 3);
         grid.sync();
         if (stamp) stamp[4] = global_ns();
         phase_apply(a, bid, nb);
+        WORK_END(ctl, 4);
         grid.sync();
         if (stamp) {
             stamp[5] = global_ns();
             __threadfence(); // read by the publishing CTA after the next barrier
         }
         upper_reduce_phase(p.bits, a.ws.dirty, p.counters, g.lc, wroot, bid, nb);
+        WORK_END(ctl, 5);
         grid.sync();
         // the frame's counters go out while the next frame's index phase is already running
         // (pool->stats may be host-mapped memory: only the launch's last frame pays for that write)
@@ -1346,6 +1431,13 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
             const ReducePublish pub = {ctl->stats, f == n_frames - 1 ? p.stats : nullptr, stats_seq, &ctl->seq_frame,
                                        ctl->phase_t[f & 1]};
             publish_frame(pub, p.counters[1], threadIdx.x);
+#ifdef CBTM_DEBUG_TIMING
+            if (threadIdx.x < CBTM_STAT_PHASES) {
+                const unsigned long long t0 = ctl->phase_t[f & 1][threadIdx.x], t1 = ctl->work_end[threadIdx.x];
+                if (stats_seq) stats_seq[(size_t)CBTM_STATS_WORDS * f + 22 + threadIdx.x] = t1 > t0 ? (int64_t)(t1 - t0) : 0;
+                ctl->work_end[threadIdx.x] = 0;
+            }
+#endif
         }
     }
 }
