@@ -67,6 +67,10 @@ extern "C" {
                                         (whole-array parity with the reference);
                                         default: only the consumed window
                                         cache_free[T - A, T) is written */
+#define CBTM_POOL_DESCEND_FREE_RANKS 4u /* resolve the frame's free ranks by tree descent (k-th unset
+                                          bit per slot) instead of through the window table -- the path
+                                          taken automatically when a frame's allocations span more than
+                                          4096 leaf blocks; the flag exists so that tests can exercise it */
 #define CBTM_POOL_STAGED_LAUNCHES 2u /* one kernel launch per pipeline stage instead of
                                         the persistent cooperative frame kernel (per-stage
                                         profiling; automatic where cooperative launch is

@@ -383,7 +383,7 @@ __device__ __forceinline__ void build_window_table(const FrameArgs &a, long long
     const Geo g = make_geo(p.depth);
     const int tid = threadIdx.x;
     if (tid == 0) ctl->win_n = 0;
-    if (T <= 0 || (p.flags & CBTM_POOL_FULL_FREE_CACHE)) return;
+    if (T <= 0 || (p.flags & (CBTM_POOL_FULL_FREE_CACHE | CBTM_POOL_DESCEND_FREE_RANKS))) return;
     uint32_t hi, before_hi;
     cta_find_free_block(p.counters, g, (uint32_t)(T - 1), scratch, s_out, hi, before_hi);
     const uint32_t lo = hi + 1 > (uint32_t)WIN_MAX ? hi + 1 - WIN_MAX : 0u;

@@ -51,7 +51,8 @@ class TriangulationState:
     """
 
     def __init__(self, mesh, depth: int, device=None,
-                 exact_free_cache: bool = False, staged_launches: bool = False):
+                 exact_free_cache: bool = False, staged_launches: bool = False,
+                 descend_free_ranks: bool = False):
         H = mesh.n_halfedges
         rank = bisector.root_rank(H)
         if depth < rank:
@@ -66,6 +67,9 @@ class TriangulationState:
         self.capacity = cap = 1 << depth
         self.exact_free_cache = bool(exact_free_cache)
         self.staged_launches = bool(staged_launches)
+        # testing hook: free ranks by tree descent instead of the window table (the fallback for
+        # frames whose allocations span more than 4096 leaf blocks)
+        self.descend_free_ranks = bool(descend_free_ranks)
         self.device = _lib.require_cuda(device)
         L = _lib.load()
         t = _lib.torch()
@@ -113,7 +117,7 @@ class TriangulationState:
     def c_pool(self) -> _lib.CPool:
         """The cbtm_pool view of this state (cached; max_depth and the mode flags
         are plain attributes a caller may change between updates)."""
-        key = (int(self.max_depth), self.exact_free_cache, self.staged_launches)
+        key = (int(self.max_depth), self.exact_free_cache, self.staged_launches, self.descend_free_ranks)
         cached = getattr(self, "_c_pool", None)
         if cached is not None and cached[0] == key:
             return cached[1]
@@ -131,7 +135,8 @@ class TriangulationState:
             p(self.d_workspace), self.d_workspace.numel(), self.depth,
             self.rank, int(self.max_depth),
             (_lib.POOL_FULL_FREE_CACHE if self.exact_free_cache else 0)
-            | (_lib.POOL_STAGED_LAUNCHES if self.staged_launches else 0))
+            | (_lib.POOL_STAGED_LAUNCHES if self.staged_launches else 0)
+            | (_lib.POOL_DESCEND_FREE_RANKS if self.descend_free_ranks else 0))
 
     def _touched(self) -> None:
         """The device arrays changed: drop host snapshots."""
@@ -240,7 +245,8 @@ class TriangulationState:
     def clone(self) -> "TriangulationState":
         other = TriangulationState(self.mesh, self.depth, device=self.device,
                                    exact_free_cache=self.exact_free_cache,
-                                   staged_launches=self.staged_launches)
+                                   staged_launches=self.staged_launches,
+                                   descend_free_ranks=self.descend_free_ranks)
         for k in ("ids", "nexts", "prevs", "twins", "commands", "reserved",
                   "cache_live", "cache_free", "counter", "bits", "counters"):
             getattr(other, "d_" + k).copy_(getattr(self, "d_" + k))
@@ -250,11 +256,12 @@ class TriangulationState:
 
 
 def initialize(mesh, depth: int, device=None, exact_free_cache: bool = False,
-               staged_launches: bool = False) -> TriangulationState:
+               staged_launches: bool = False, descend_free_ranks: bool = False) -> TriangulationState:
     """One root bisector per halfedge at slots [0, H) (state.py:139-156)."""
     st = TriangulationState(mesh, depth, device=device,
                             exact_free_cache=exact_free_cache,
-                            staged_launches=staged_launches)
+                            staged_launches=staged_launches,
+                            descend_free_ranks=descend_free_ranks)
     pool = st.c_pool()
     rc = _lib.load().cbtm_initialize(
         C.byref(pool), _lib.ptr(st.d_he_next), _lib.ptr(st.d_he_prev),

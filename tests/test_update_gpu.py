@@ -18,17 +18,20 @@ from tests.parity import (assert_state_equal, golden_frame_check, load_golden,
 pytestmark = pytest.mark.gpu
 
 
-MODES = ["exact", "fast", "fast-staged", "exact-staged"]
+MODES = ["exact", "fast", "fast-staged", "exact-staged", "fast-descend"]
 
 
 def run_pair(name, mesh, depth, frames, gpu_decide_of, orc_verdict_of, mode,
              max_depth=None, golden=True, check_every=1):
     """mode: exact = whole free cache materialised (whole-array parity);
     fast = only the consumed free-rank window; -staged = one kernel per stage
-    instead of the persistent cooperative frame kernel."""
+    instead of the persistent cooperative frame kernel; -descend = free ranks
+    resolved by tree descent instead of the window table (the fallback taken
+    when a frame's allocations span more than 4096 leaf blocks)."""
     from oracle import OraclePool
     exact = mode.startswith("exact")
-    st = initialize(mesh, depth, exact_free_cache=exact, staged_launches=mode.endswith("staged"))
+    st = initialize(mesh, depth, exact_free_cache=exact, staged_launches=mode.endswith("staged"),
+                    descend_free_ranks=mode.endswith("descend"))
     op = OraclePool(mesh, depth)
     if max_depth is not None:
         st.max_depth = max_depth
@@ -115,7 +118,7 @@ def test_config2_cube_sphere_flyin_exact():
     run_pair("cube_sphere_flyin_d20", seq.mesh, 20, seq.n_frames, g, o, "exact")
 
 
-@pytest.mark.parametrize("mode", ["fast", "fast-staged"])
+@pytest.mark.parametrize("mode", ["fast", "fast-staged", "fast-descend"])
 def test_config2_cube_sphere_flyin_fast(mode):
     seq = workloads.cube_sphere_flyin(depth=20, frames=64)
     g, o = _lod_pair(seq)
@@ -187,3 +190,21 @@ def test_batch_kernel_equals_separate_sequences():
         ha, hb = solo[p].to_host(), both[p].to_host()
         for k in ha:
             assert np.array_equal(ha[k], hb[k]), f"planet {p}: {k}"
+
+
+def test_more_planets_than_one_launch_takes():
+    """Eleven small planets: the batch API splits them into launches of at most
+    MAX_BATCH pools; results equal separate runs."""
+    from paper_2407_02215_b200 import _lib
+    from paper_2407_02215_b200.pipeline import run_lod_sequence_batch
+    assert _lib.MAX_BATCH < 11
+    seqs = [workloads.cube_sphere_flyin(depth=13 + p % 3, frames=10) for p in range(11)]
+    solo = [initialize(s.mesh, s.depth) for s in seqs]
+    both = [initialize(s.mesh, s.depth) for s in seqs]
+    with ParallelEngine() as eng:
+        want = [eng.run_lod_sequence(st, s.params()) for st, s in zip(solo, seqs)]
+    got = run_lod_sequence_batch(both, [s.params() for s in seqs])
+    for p in range(11):
+        assert [stats_words(s) for s in want[p]] == [stats_words(s) for s in got[p]], p
+        assert np.array_equal(solo[p].to_host()["nodes"], both[p].to_host()["nodes"]), p
+        assert np.array_equal(solo[p].ids, both[p].ids), p
