@@ -429,6 +429,10 @@ __device__ __forceinline__ void walk_split_chain(const cbtm_pool &p, int32_t s)
     // Pointer fields do not change during this phase, so the twin's operators
     // are fetched while the atomic on `cur` is still in flight, and the twin's
     // twin doubles as the next hop's twin: one dependent round trip per hop.
+    // The old value of the atomic must be honoured BEFORE the next node is
+    // touched: "T already set" means "whoever set it walks the rest of the
+    // chain", which only holds if nobody marks a node and then stops (a variant
+    // that looked at the old value one hop late lost parts of chains).
     int32_t cur = s;
     int32_t t = p.twins[cur];
     for (int hops = 0;;) {
