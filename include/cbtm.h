@@ -233,6 +233,16 @@ int cbtm_classify(const cbtm_pool *pool, const cbtm_verdict *verdict, int8_t *ve
 int cbtm_decode_triangles(const uint64_t *ids, int64_t K, int32_t rank,
                           const double *root_tris, double *out, uintptr_t stream);
 
+/* ---- state.decode_live (state.py:104-113) without the host: re-indexes the pool (cache_live :=
+ *      active list of the current state, ascending slot order) and decodes every live bisector
+ *      into out f64[min(n, out_capacity)*9] in that order; n is read from the CBT root on the
+ *      device.  draw_args (device u32[4], may be NULL) receives the indirect draw arguments
+ *      {3 * triangles, 1, 0, 0} -- the step that follows the update in the paper's frame
+ *      (PAPER.md:1126-1128).  Note: it overwrites cache_live[0, n) like stage 2 of the next
+ *      update would. */
+int cbtm_export_live_triangles(const cbtm_pool *pool, const double *root_tris, double *out,
+                               int64_t out_capacity, uint32_t *draw_args, uintptr_t stream);
+
 /* ---- pointer_violations (state.py:169-203) as a device-side check, so that a
  *      parity failure can be localised without downloading the pool.  out is
  *      device i64[CBTM_VALIDATE_WORDS] = {live slots, ids below the root range or

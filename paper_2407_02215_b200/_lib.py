@@ -87,6 +87,7 @@ SIGNATURES = {
     "cbtm_root_triangles": (C.c_int, [_P, _P, _P, C.c_int32, _P, _UP]),
     "cbtm_classify": (C.c_int, [C.POINTER(CPool), C.POINTER(CVerdict), _P, _UP]),
     "cbtm_decode_triangles": (C.c_int, [_P, _I64, C.c_int32, _P, _P, _UP]),
+    "cbtm_export_live_triangles": (C.c_int, [C.POINTER(CPool), _P, _P, _I64, _P, _UP]),
     "cbtm_validate": (C.c_int, [C.POINTER(CPool), C.c_int32, _P, _UP]),
     "cbtm_update": (C.c_int, [C.POINTER(CPool), C.POINTER(CVerdict), _UP]),
     "cbtm_update_begin": (C.c_int, [C.POINTER(CPool), _UP]),

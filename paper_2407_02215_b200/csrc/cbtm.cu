@@ -348,6 +348,27 @@ int cbtm_decode_triangles(const uint64_t *ids, int64_t K, int32_t rank, const do
     return launch_status();
 }
 
+int cbtm_export_live_triangles(const cbtm_pool *pool, const double *root_tris, double *out, int64_t out_capacity,
+                               uint32_t *draw_args, uintptr_t stream)
+{
+    int rc = check_pool(pool, false);
+    if (rc) return rc;
+    if (!root_tris || !out) return CBTM_E_NULL;
+    if (out_capacity < 0) return CBTM_E_RANGE;
+    cudaStream_t st = as_stream(stream);
+    // the active list of the CURRENT state (an update leaves the list of the state it started from)
+    k_index<false><<<strided_grid(make_geo(pool->depth).nblocks, IDX_WARPS, 6), IDX_WARPS * 32, 0, st>>>(
+        reinterpret_cast<const uint32_t *>(pool->bits), pool->counters, pool->depth, pool->cache_live, nullptr,
+        pool->dispatch, nullptr);
+    rc = launch_status();
+    if (rc) return rc;
+    const uint64_t cap = (uint64_t)out_capacity < ((uint64_t)1 << pool->depth) ? (uint64_t)out_capacity
+                                                                               : ((uint64_t)1 << pool->depth);
+    k_export_live_triangles<<<strided_grid(cap ? cap : 1, 256, 8), 256, 0, st>>>(
+        pool->ids, pool->cache_live, pool->counters, pool->rank, root_tris, out, (uint64_t)out_capacity, draw_args);
+    return launch_status();
+}
+
 int cbtm_validate(const cbtm_pool *pool, int32_t n_halfedges, int64_t *out, uintptr_t stream)
 {
     int rc = check_pool(pool, false);

@@ -175,4 +175,29 @@ k_decode_triangles(const uint64_t *__restrict__ ids, int64_t K, int rank,
     }
 }
 
+// The step right after the update in the paper's frame: all live
+// bisectors decoded into a vertex buffer, in active-list order, with the indirect draw
+// arguments written on the device -- n is read from the CBT root, nothing goes through
+// the host.  cache_live must be current (cbtm_index, or any update followed by an index).
+__global__ void __launch_bounds__(256)
+k_export_live_triangles(const uint64_t *__restrict__ ids, const int32_t *__restrict__ cache_live,
+                        const uint32_t *__restrict__ counters, int rank, const double *__restrict__ root_tris,
+                        double *__restrict__ out, uint64_t out_capacity, uint32_t *__restrict__ draw_args)
+{
+    const uint32_t n = counters[1];
+    const uint64_t m = n < out_capacity ? n : out_capacity;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && draw_args) {
+        draw_args[0] = 3u * (uint32_t)m; // vertex count
+        draw_args[1] = 1;               // instance count
+        draw_args[2] = 0;               // first vertex
+        draw_args[3] = 0;               // first instance
+    }
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        double t[9];
+        decode_triangle(ids[cache_live[i]], rank, root_tris, t);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) out[9 * i + k] = t[k];
+    }
+}
+
 } // namespace cbtm

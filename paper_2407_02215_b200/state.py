@@ -209,18 +209,31 @@ class TriangulationState:
         return [(int(i), t) for i, t in zip(ids, tris)]
 
     def decode_live(self) -> tuple[np.ndarray, np.ndarray]:
-        """(ids, (n, 3, 3) fp64 vertices) of all live bisectors, decoded on the
-        GPU (cbtm_decode_triangles; reference: state.py:104-113)."""
+        """(ids, (n, 3, 3) fp64 vertices) of all live bisectors in ascending
+        slot order, decoded on the GPU (reference: state.py:104-113)."""
+        d_tris, _ = self.export_live_triangles()
+        n = d_tris.shape[0]
         t = _lib.torch()
-        slots = t.from_numpy(self.live_slots().astype(np.int64)).to(self.device)
-        d_ids = self.d_ids[slots].contiguous()
-        out = t.empty((d_ids.numel(), 3, 3), dtype=t.float64, device=self.device)
-        if d_ids.numel():
-            rc = _lib.load().cbtm_decode_triangles(
-                _lib.ptr(d_ids), d_ids.numel(), self.rank,
-                _lib.ptr(self.d_root_tris), _lib.ptr(out), self.stream())
-            _lib.check(rc, "cbtm_decode_triangles")
-        return _lib.to_host(d_ids, np.uint64), _lib.to_host(out)
+        d_ids = self.d_ids[self.d_cache_live[:n].to(t.int64)]
+        return _lib.to_host(d_ids, np.uint64), _lib.to_host(d_tris)
+
+    def export_live_triangles(self, out=None):
+        """Device-resident triangle export (cbtm_export_live_triangles): returns
+        (float64[n, 3, 3] CUDA tensor of the live bisectors' vertices in active-list
+        order, int32[4] CUDA tensor with the indirect draw arguments).  Nothing but
+        the live count crosses to the host (to size the returned view); pass a
+        preallocated ``out`` (float64[capacity, 3, 3]) to avoid even the allocation."""
+        t = _lib.torch()
+        n = self.count()
+        if out is None:
+            out = t.empty((max(n, 1), 3, 3), dtype=t.float64, device=self.device)
+        draw = t.zeros(4, dtype=t.int32, device=self.device)
+        pool = self.c_pool()
+        rc = _lib.load().cbtm_export_live_triangles(C.byref(pool), _lib.ptr(self.d_root_tris), _lib.ptr(out),
+                                                    out.shape[0], _lib.ptr(draw), self.stream())
+        _lib.check(rc, "cbtm_export_live_triangles")
+        self._version += 1  # cache_live now lists the current state
+        return out[:min(n, out.shape[0])], draw
 
     def validate_device(self) -> dict:
         """Counts of structural violations over the live pool, computed on the

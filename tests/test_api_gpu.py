@@ -182,6 +182,19 @@ def test_triangle_export_matches_host_decode():
     roots = np.array([st.mesh.root_bisector_vertices(h) for h in range(60)])
     root_area = 0.5 * np.linalg.norm(np.cross(roots[:, 1] - roots[:, 0], roots[:, 2] - roots[:, 0]), axis=1).sum()
     assert abs(area - root_area) < 1e-9
+    # device-resident export: same triangles in active-list (ascending slot) order, draw args on device,
+    # and the active list it leaves behind is the current state's
+    d_tris, d_draw = st.export_live_triangles()
+    assert np.array_equal(d_tris.cpu().numpy().view(np.uint64), tris.view(np.uint64))
+    assert d_draw.cpu().tolist() == [3 * len(ids), 1, 0, 0]
+    assert np.array_equal(st.cache_live[:len(ids)], st.live_slots())
+    assert np.array_equal(st.ids[st.live_slots()], ids)
+    # a too small output buffer truncates instead of overrunning
+    import torch
+    small = torch.full((100, 3, 3), -1.0, dtype=torch.float64, device=st.device)
+    part, d_draw = st.export_live_triangles(out=small)
+    assert part.shape[0] == 100 and d_draw.cpu().tolist() == [300, 1, 0, 0]
+    assert np.array_equal(part.cpu().numpy().view(np.uint64), tris[:100].view(np.uint64))
 
 
 def test_device_validator_reports_corruption():
