@@ -66,3 +66,36 @@ def test_no_cpu_fallback():
         Cbt(4)
     with pytest.raises(_lib.CbtmError):
         initialize(halfedge.single_quad(), 8)
+    with pytest.raises(_lib.CbtmError):   # the device mesh ingest has no host fallback either
+        halfedge.from_polygons_device(*_quad_polygons())
+
+
+def _quad_polygons():
+    from paper_2407_02215_b200 import halfedge
+    m = halfedge.single_quad()
+    return m.positions, [[int(v) for v in m.vert]]
+
+
+def test_new_entry_points_check_their_arguments(lib):
+    """Contract violations of the round-1c entry points are reported before anything is launched."""
+    assert lib.cbtm_wait_frame(None, 1, 1000) == 2                       # CBTM_E_NULL
+    import numpy as np
+    stats = np.zeros(_lib.STATS_WORDS, dtype=np.int64)
+    assert lib.cbtm_wait_frame(stats.ctypes.data, 1, 2_000_000) == 7     # CBTM_E_TIMEOUT after 2 ms
+    stats[_lib.STAT_SEQ] = 5
+    assert lib.cbtm_wait_frame(stats.ctypes.data, 5, 1000) == 0          # already there: no spinning
+    assert lib.cbtm_run_lod_sequence_batch(None, 1, None, None, 1, None, 0) == 2
+    pools = (_lib.CPool * 1)()
+    ptrs = (C.c_void_p * 1)(1)
+    assert lib.cbtm_run_lod_sequence_batch(pools, 0, ptrs, ptrs, 1, None, 0) == 5    # CBTM_E_RANGE
+    assert lib.cbtm_run_lod_sequence_batch(pools, _lib.MAX_BATCH + 1, ptrs, ptrs, 1, None, 0) == 5
+    assert lib.cbtm_mesh_workspace_bytes(0) == 0 and lib.cbtm_mesh_workspace_bytes(240) > 0
+    assert lib.cbtm_mesh_from_polygons(*([None] * 2), 1, 3, 3, *([None] * 8), 0, 0) == 2
+    assert lib.cbtm_export_live_triangles(None, None, None, 0, None, 0) == 2
+
+
+def test_batch_api_validates_before_touching_the_gpu():
+    from paper_2407_02215_b200.pipeline import run_lod_sequence_batch
+    assert run_lod_sequence_batch([], []) == []
+    with pytest.raises(ValueError):
+        run_lod_sequence_batch([object()], [])
