@@ -461,23 +461,32 @@ __device__ __forceinline__ void walk_split_chain(const cbtm_pool &p, int32_t s)
     }
 }
 
-__device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t bid, uint32_t nb)
+__device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb)
 {
     __shared__ double prm[CBTM_PRM_WORDS];
     __shared__ uint32_t wsum[CHUNK / 32], wmin[CHUNK / 32];
     const cbtm_pool &p = a.pool;
     Control *ctl = a.ws.ctl;
-    const uint32_t n = p.counters[1];
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
     const bool fast = fits_a_priori(p, n); // nothing can be rejected: scatter right away
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    load_prm(a, prm);
+    // the camera parameters of a sequence run sit behind two dependent loads (frame index, then
+    // the row): issued now, parked in a register, put into shared memory only when the first
+    // verdict needs them -- the record gathers below run meanwhile
+    double prm_reg = 0.0;
+    bool prm_pending = a.vmode == CBTM_VERDICT_LOD;
+    if (prm_pending && tid < CBTM_PRM_WORDS)
+        prm_reg = a.use_prm_seq ? a.ws.prm_seq[(size_t)CBTM_PRM_WORDS * ctl->seq_frame + tid] : a.prm[tid];
 
     for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
         const uint32_t i = chunk * CHUNK + tid;
         uint32_t need = 0, mbits = 0;
         int32_t s = -1;
+        struct {
+            uint64_t id, js, jo;
+            int32_t sib, oth, j4, nx, pv;
+        } gathered = {0, 0, 0, -1, -1, -1, -1, -1};
         if (i < n) {
             s = p.cache_live[i];
             const uint64_t id = p.ids[s];
@@ -493,6 +502,16 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t bid,
                 jo = p.ids[oth];
                 j4 = odd ? p.nexts[oth] : p.prevs[oth];
             }
+            gathered = {id, js, jo, sib, oth, j4, nx, pv};
+        }
+        if (prm_pending) { // CTA-uniform
+            if (tid < CBTM_PRM_WORDS) prm[tid] = prm_reg;
+            __syncthreads();
+            prm_pending = false;
+        }
+        if (i < n) {
+            const uint64_t id = gathered.id, js = gathered.js, jo = gathered.jo;
+            const int32_t sib = gathered.sib, oth = gathered.oth, j4 = gathered.j4;
             const int v = verdict_of(a, prm, id, i);
             if (v == 1) {
                 const int d = depth_of(id, p.rank);
@@ -551,12 +570,11 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t bid,
 // Fast path, admin CTA: T = total need once every chunk has reported (waits for
 // the other CTAs' chunks, so a CTA with chunks of several pools calls it only
 // after all of them), then the window table.
-__device__ __forceinline__ void phase_classify_admin(const FrameArgs &a)
+__device__ __forceinline__ void phase_classify_admin(const FrameArgs &a, uint32_t n)
 {
     __shared__ unsigned long long s_total;
     const cbtm_pool &p = a.pool;
     Control *ctl = a.ws.ctl;
-    const uint32_t n = p.counters[1];
     if (!fits_a_priori(p, n)) return;
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
     if (threadIdx.x == 0) {
@@ -780,11 +798,10 @@ __device__ __forceinline__ void phase_scatter(const FrameArgs &a, uint32_t bid, 
 // live slot (merge_ref: owner and pair of every agreed-merge member) and count
 // each rank's allocations (kernels.py:347-368).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t bid, uint32_t nb)
+__device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb)
 {
     __shared__ uint32_t wsum[CHUNK / 32];
     const cbtm_pool &p = a.pool;
-    const uint32_t n = (uint32_t)a.ws.ctl->n;
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
@@ -871,7 +888,7 @@ __device__ __forceinline__ uint64_t cta_range_sum(const uint32_t *v, uint32_t lo
 // then just picks its slots; outside the table (fragmented pool) each thread
 // descends the tree.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t bid, uint32_t nb)
+__device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb)
 {
     __shared__ uint32_t scratch[32];
     __shared__ unsigned long long scratch64[CHUNK / 32];
@@ -880,7 +897,6 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t bid, 
     const cbtm_pool &p = a.pool;
     Control *ctl = a.ws.ctl;
     const Geo g = make_geo(p.depth);
-    const uint32_t n = (uint32_t)ctl->n;
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
     const long long T = ctl->T;
     const bool full = p.flags & CBTM_POOL_FULL_FREE_CACHE;
@@ -888,7 +904,7 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t bid, 
     const uint32_t *bits32 = reinterpret_cast<const uint32_t *>(p.bits);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t win_n = ctl->win_n, win_lo = ctl->win_lo; // CTA-uniform: written before the last barrier
-    const uint32_t win_first = win_n ? win[0] : 0u;
+    const uint32_t win_first = win[0]; // (garbage while win_n == 0, never used then)
 
     long long off = 0;      // slots allocated by chunks [0, summed)
     uint32_t summed = 0;
@@ -934,6 +950,7 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t bid, 
                 const uint32_t c = __popc(z);
                 uint32_t r = first + warp_inclusive_scan(c) - c; // free rank of this lane's first free slot
                 const int32_t lane_base = (int32_t)(b * g.span + lane * 32);
+                if (r + c <= lo_rank || r >= hi_rank) z = 0; // none of this word's free slots is wanted
                 while (z) {
                     const int k = __ffs(z) - 1;
                     z &= z - 1;
@@ -1245,11 +1262,10 @@ __device__ __forceinline__ void apply_merged_pair(ApplyCtx &cx, int32_t e, int32
     if (q_ext.slot >= 0 && survives(q_ext)) redirect_to(p, q_ext, e, par, E_NEXT);
 }
 
-__device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t bid, uint32_t nb)
+__device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb)
 {
     __shared__ uint32_t acc[5];
     const cbtm_pool &p = a.pool;
-    const uint32_t n = (uint32_t)a.ws.ctl->n;
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
     const int tid = threadIdx.x;
     if (tid < 5) acc[tid] = 0;
@@ -1332,8 +1348,9 @@ __global__ void __launch_bounds__(CHUNK) k_reset(const __grid_constant__ FrameAr
 // must all be resident (the host sizes this grid from the kernel's occupancy)
 __global__ void __launch_bounds__(CHUNK) k_classify_frame(const __grid_constant__ FrameArgs a)
 {
-    phase_classify(a, blockIdx.x, gridDim.x);
-    if (blockIdx.x == gridDim.x - 1) phase_classify_admin(a);
+    const uint32_t n = a.pool.counters[1];
+    phase_classify(a, n, blockIdx.x, gridDim.x);
+    if (blockIdx.x == gridDim.x - 1) phase_classify_admin(a, n);
 }
 
 __global__ void __launch_bounds__(CHUNK) k_admit(const __grid_constant__ FrameArgs a)
@@ -1348,17 +1365,17 @@ __global__ void __launch_bounds__(CHUNK) k_scatter(const __grid_constant__ Frame
 
 __global__ void __launch_bounds__(CHUNK) k_agree(const __grid_constant__ FrameArgs a)
 {
-    phase_agree(a, blockIdx.x, gridDim.x);
+    phase_agree(a, (uint32_t)a.ws.ctl->n, blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(CHUNK) k_reserve(const __grid_constant__ FrameArgs a)
 {
-    phase_reserve(a, blockIdx.x, gridDim.x);
+    phase_reserve(a, (uint32_t)a.ws.ctl->n, blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(CHUNK) k_apply(const __grid_constant__ FrameArgs a)
 {
-    phase_apply(a, blockIdx.x, gridDim.x);
+    phase_apply(a, (uint32_t)a.ws.ctl->n, blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(CHUNK) k_publish(const __grid_constant__ FrameArgs a, int64_t *stats_seq)
@@ -1399,9 +1416,10 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         WORK_END(ctl, 0);
         grid.sync();
         if (stamp) stamp[1] = global_ns();
-        const bool fast = fits_a_priori(p, p.counters[1]); // grid-uniform
-        phase_classify(a, bid, nb);
-        if (bid == nb - 1) phase_classify_admin(a);
+        const uint32_t n = p.counters[1];      // the frame's live count: one read per CTA, kept in a register
+        const bool fast = fits_a_priori(p, n); // grid-uniform
+        phase_classify(a, n, bid, nb);
+        if (bid == nb - 1) phase_classify_admin(a, n);
         WORK_END(ctl, 1);
         grid.sync();
         if (!fast) { // pool under reservation pressure: one CTA admits, then everybody scatters
@@ -1411,15 +1429,15 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
             grid.sync();
         }
         if (stamp) stamp[2] = global_ns();
-        phase_agree(a, bid, nb);
+        phase_agree(a, n, bid, nb);
         WORK_END(ctl, 2);
         grid.sync();
         if (stamp) stamp[3] = global_ns();
-        phase_reserve(a, bid, nb);
+        phase_reserve(a, n, bid, nb);
         WORK_END(ctl, 3);
         grid.sync();
         if (stamp) stamp[4] = global_ns();
-        phase_apply(a, bid, nb);
+        phase_apply(a, n, bid, nb);
         WORK_END(ctl, 4);
         grid.sync();
         if (stamp) {
@@ -1495,12 +1513,12 @@ k_frames_batch(const __grid_constant__ BatchArgs b, int n_pools, int n_frames)
         bool any_slow = false; // grid-uniform
         for (int q = 0; q < n_pools; ++q) {
             any_slow |= !fits_a_priori(b.a[q].pool, b.a[q].pool.counters[1]);
-            phase_classify(b.a[q], vbid(q), nb);
+            phase_classify(b.a[q], b.a[q].pool.counters[1], vbid(q), nb);
             __syncthreads();
         }
         for (int q = 0; q < n_pools; ++q) // admin duties last: they wait for the other CTAs' chunks
             if (vbid(q) == nb - 1) {
-                phase_classify_admin(b.a[q]);
+                phase_classify_admin(b.a[q], b.a[q].pool.counters[1]);
                 __syncthreads();
             }
         grid.sync();
@@ -1517,19 +1535,19 @@ k_frames_batch(const __grid_constant__ BatchArgs b, int n_pools, int n_frames)
         }
         stamp(f, 2);
         for (int q = 0; q < n_pools; ++q) {
-            phase_agree(b.a[q], vbid(q), nb);
+            phase_agree(b.a[q], (uint32_t)b.a[q].ws.ctl->n, vbid(q), nb);
             __syncthreads();
         }
         grid.sync();
         stamp(f, 3);
         for (int q = 0; q < n_pools; ++q) {
-            phase_reserve(b.a[q], vbid(q), nb);
+            phase_reserve(b.a[q], (uint32_t)b.a[q].ws.ctl->n, vbid(q), nb);
             __syncthreads();
         }
         grid.sync();
         stamp(f, 4);
         for (int q = 0; q < n_pools; ++q) {
-            phase_apply(b.a[q], vbid(q), nb);
+            phase_apply(b.a[q], (uint32_t)b.a[q].ws.ctl->n, vbid(q), nb);
             __syncthreads();
         }
         grid.sync();
