@@ -329,8 +329,8 @@ __device__ __forceinline__ uint32_t recount_block(const uint64_t *bits, uint32_t
 }
 
 __device__ __forceinline__ void upper_reduce_phase(const uint64_t *bits, uint8_t *dirty, uint32_t *counters,
-                                                   int lc, uint32_t (*wroot)[RED_THREADS / 32], uint32_t bid,
-                                                   uint32_t nb)
+                                                   int lc, uint32_t *tile_vals /* UP_TILE words of shared memory */,
+                                                   uint32_t (*wroot)[RED_THREADS / 32], uint32_t bid, uint32_t nb)
 {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint32_t nblocks = 1u << lc;
@@ -341,41 +341,43 @@ __device__ __forceinline__ void upper_reduce_phase(const uint64_t *bits, uint8_t
     };
     uint32_t k = 0;
     for (uint32_t tile = bid; tile < n_tiles; tile += nb, ++k) {
-        const uint32_t first = tile * UP_TILE + 4u * t;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        uint32_t d4 = 0, old_root = 0;
-        if (first + 4u <= nblocks) {
-            v = *reinterpret_cast<const uint4 *>(counters + nblocks + first);
-            d4 = *reinterpret_cast<const uint32_t *>(dirty + first);
-        } else if (first < nblocks) { // pools of 1 or 2 leaf blocks
-            v.x = counters[nblocks + first];
-            d4 = dirty[first];
-            if (first + 1 < nblocks) {
-                v.y = counters[nblocks + first + 1];
-                d4 |= (uint32_t)dirty[first + 1] << 8;
+        // Recount: a frame's fresh slots fall into a run of CONSECUTIVE leaf blocks, so for this step a
+        // thread owns the blocks t, t + 256, t + 512, t + 768 of the tile (a dense run of marks then
+        // spreads over different threads and their recounts run in parallel, one round trip), and the
+        // values change hands through shared memory for the tree, where a thread owns four siblings.
+        const uint32_t base = tile * UP_TILE;
+        uint32_t c[4] = {0, 0, 0, 0};
+        uint32_t d[4] = {0, 0, 0, 0};
+        uint32_t old_root = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t b = base + t + q * RED_THREADS;
+            if (b < nblocks) {
+                c[q] = counters[nblocks + b];
+                d[q] = dirty[b];
             }
         }
         // the tile root as the levels above still see it (rewritten below by this same thread)
         if (n_tiles > 1 && t == 0) old_root = counters[(1u << top) + tile];
-        if (d4) { // leaf blocks touched by this frame recount their line
-            if (d4 & 0x000000ffu) counters[nblocks + first] = v.x = recount_block(bits, first);
-            if (d4 & 0x0000ff00u) counters[nblocks + first + 1] = v.y = recount_block(bits, first + 1);
-            if (d4 & 0x00ff0000u) counters[nblocks + first + 2] = v.z = recount_block(bits, first + 2);
-            if (d4 & 0xff000000u) counters[nblocks + first + 3] = v.w = recount_block(bits, first + 3);
-            if (first + 4u <= nblocks)
-                *reinterpret_cast<uint32_t *>(dirty + first) = 0u;
-            else {
-                dirty[first] = 0;
-                if (first + 1 < nblocks) dirty[first + 1] = 0;
-            }
-        }
         // a tile without a touched block keeps all its counters
-        if (!__syncthreads_or(d4 != 0)) continue;
-        const uint32_t a0 = v.x + v.y, a1 = v.z + v.w, c = a0 + a1;
+        if (!__syncthreads_or((d[0] | d[1] | d[2] | d[3]) != 0)) continue;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t b = base + t + q * RED_THREADS;
+            if (d[q]) {
+                c[q] = recount_block(bits, b);
+                counters[nblocks + b] = c[q];
+                dirty[b] = 0;
+            }
+            tile_vals[t + q * RED_THREADS] = c[q];
+        }
+        __syncthreads();
+        const uint4 v = *reinterpret_cast<const uint4 *>(tile_vals + 4 * t);
+        const uint32_t a0 = v.x + v.y, a1 = v.z + v.w, cc = a0 + a1;
         put(lc - 1, tile * 512 + 2 * t, a0);
         put(lc - 1, tile * 512 + 2 * t + 1, a1);
-        put(lc - 2, tile * 256 + t, c);
-        const uint32_t l1 = c + __shfl_xor_sync(FULL_MASK, c, 1);
+        put(lc - 2, tile * 256 + t, cc);
+        const uint32_t l1 = cc + __shfl_xor_sync(FULL_MASK, cc, 1);
         const uint32_t l2 = l1 + __shfl_xor_sync(FULL_MASK, l1, 2);
         const uint32_t l3 = l2 + __shfl_xor_sync(FULL_MASK, l2, 4);
         const uint32_t l4 = l3 + __shfl_xor_sync(FULL_MASK, l3, 8);
@@ -386,7 +388,7 @@ __device__ __forceinline__ void upper_reduce_phase(const uint64_t *bits, uint8_t
         else if ((lane & 15) == 7) put(lc - 6, tile * 16 + warp * 2 + (lane >> 4), l4);
         else if (lane == 15) put(lc - 7, tile * 8 + warp, l5);
         if (lane == 0) wroot[k & 1][warp] = l5;
-        __syncthreads();
+        __syncthreads(); // (also: tile_vals may be refilled by the next tile)
         if (warp == 0 && lane < 7) {
             const uint32_t *w = wroot[k & 1];
             if (lane < 4) put(lc - 8, tile * 4 + lane, w[2 * lane] + w[2 * lane + 1]);
@@ -410,8 +412,9 @@ __device__ __forceinline__ void upper_reduce_phase(const uint64_t *bits, uint8_t
 __global__ void __launch_bounds__(RED_THREADS)
 k_upper_reduce(const uint64_t *bits, uint8_t *dirty, uint32_t *counters, int lc)
 {
+    __shared__ __align__(16) uint32_t tile_vals[UP_TILE];
     __shared__ uint32_t wroot[2][RED_THREADS / 32];
-    upper_reduce_phase(bits, dirty, counters, lc, wroot, blockIdx.x, gridDim.x);
+    upper_reduce_phase(bits, dirty, counters, lc, tile_vals, wroot, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------

@@ -1444,7 +1444,7 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
             stamp[5] = global_ns();
             __threadfence(); // read by the publishing CTA after the next barrier
         }
-        upper_reduce_phase(p.bits, a.ws.dirty, p.counters, g.lc, wroot, bid, nb);
+        upper_reduce_phase(p.bits, a.ws.dirty, p.counters, g.lc, reinterpret_cast<uint32_t *>(dyn_smem), wroot, bid, nb);
         WORK_END(ctl, 5);
         grid.sync();
         // the frame's counters go out while the next frame's index phase is already running
@@ -1555,7 +1555,8 @@ k_frames_batch(const __grid_constant__ BatchArgs b, int n_pools, int n_frames)
         if (bid == 0 && threadIdx.x == 0) __threadfence();
         for (int q = 0; q < n_pools; ++q) {
             const cbtm_pool &p = b.a[q].pool;
-            upper_reduce_phase(p.bits, b.a[q].ws.dirty, p.counters, make_geo(p.depth).lc, wroot, vbid(q), nb);
+            upper_reduce_phase(p.bits, b.a[q].ws.dirty, p.counters, make_geo(p.depth).lc,
+                               reinterpret_cast<uint32_t *>(dyn_smem), wroot, vbid(q), nb);
             __syncthreads();
         }
         grid.sync();
