@@ -1052,6 +1052,8 @@ struct Neighbour {
     int32_t tw, nx, pv;
     int4 res;         // its reservation (final since k_reserve)
     int32_t mref;     // its agreed-merge reference (k_agree), -1 if none
+    int32_t parent;   // slot of the parent that replaces it if it is a member of an agreed merge
+                      // (resolve_parent; one more dependent load, issued for all neighbours together)
 };
 
 struct ApplyCtx {
@@ -1067,10 +1069,11 @@ __device__ __forceinline__ Neighbour load_neighbour(const ApplyCtx &cx, int32_t 
     nbr.slot = slot;
     if (slot < 0) {
         nbr.cmd = 0;
-        nbr.tw = nbr.nx = nbr.pv = nbr.mref = -1;
+        nbr.tw = nbr.nx = nbr.pv = nbr.mref = nbr.parent = -1;
         nbr.res = make_int4(-1, -1, -1, -1);
         return nbr;
     }
+    nbr.parent = -1;
     const cbtm_pool &p = cx.p;
     nbr.cmd = p.commands[slot];
     nbr.tw = p.twins[slot];
@@ -1079,6 +1082,18 @@ __device__ __forceinline__ Neighbour load_neighbour(const ApplyCtx &cx, int32_t 
     nbr.res = *reinterpret_cast<const int4 *>(p.reserved + 4 * (size_t)slot);
     nbr.mref = cx.merge_ref[slot];
     return nbr;
+}
+
+// kernels.py:183-191 / 159-180: does the neighbour vanish into an agreed merge?
+__device__ __forceinline__ bool merges_away(const Neighbour &t)
+{
+    return t.slot >= 0 && !(t.cmd & CBTM_CMD_SPLIT_MASK) && (t.cmd & CBTM_CMD_MERGE) && t.mref >= 0;
+}
+
+// parent slot held by the merge owner; call it for all neighbours before using any result
+__device__ __forceinline__ void resolve_parent(const ApplyCtx &cx, Neighbour &t)
+{
+    if (merges_away(t)) t.parent = cx.p.reserved[4 * (size_t)(t.mref >> 1) + (t.mref & 1)];
 }
 
 __device__ __forceinline__ int32_t pick4(const int4 &v, int idx)
@@ -1117,8 +1132,7 @@ __device__ __forceinline__ int32_t piece_of(ApplyCtx &cx, const Neighbour &t, in
         }
         return pick4(t.res, idx);
     }
-    if ((t.cmd & CBTM_CMD_MERGE) && t.mref >= 0) // parent slot held by the merge owner (kernels.py:159-180)
-        return cx.p.reserved[4 * (size_t)(t.mref >> 1) + (t.mref & 1)];
+    if ((t.cmd & CBTM_CMD_MERGE) && t.mref >= 0) return t.parent; // kernels.py:159-180 (resolve_parent)
     return t.slot;
 }
 
@@ -1192,47 +1206,57 @@ __device__ __forceinline__ void apply_split(ApplyCtx &cx, int32_t s, uint32_t sm
     const uint64_t j = own.id;
     const int32_t nb_n = own.nx, nb_p = own.pv, nb_t = own.tw;
     const int4 r4 = own.res;
-    const Neighbour tn = load_neighbour(cx, nb_n), tp = load_neighbour(cx, nb_p), tt = load_neighbour(cx, nb_t);
+    // round trip: the three neighbour bundles; round trip: the parents of those that merge away;
+    // only then is anything consumed or stored (a store in between would serialise the loads)
+    Neighbour tn = load_neighbour(cx, nb_n), tp = load_neighbour(cx, nb_p), tt = load_neighbour(cx, nb_t);
+    resolve_parent(cx, tn);
+    resolve_parent(cx, tp);
+    resolve_parent(cx, tt);
     const bool split_p = sm & CBTM_CMD_SPLIT_P, split_n = sm & CBTM_CMD_SPLIT_N;
     const int left_n = split_p ? 2 : 1;
     const int32_t left_last = split_p ? r4.y : r4.x;
     const int32_t right_first = split_p ? r4.z : r4.y;
     const int32_t right_second = split_p ? r4.w : r4.z;
+    const int32_t t_v0 = piece_of(cx, tt, E_TWIN, H_V0, s), t_v1 = piece_of(cx, tt, E_TWIN, H_V1, s);
+    const int32_t p_a = piece_of(cx, tp, E_PREV, split_p ? H_V0 : H_WHOLE, s);
+    const int32_t p_b = split_p ? piece_of(cx, tp, E_PREV, H_V2, s) : -1;
+    const int32_t n_a = piece_of(cx, tn, E_NEXT, split_n ? H_V2 : H_WHOLE, s);
+    const int32_t n_b = split_n ? piece_of(cx, tn, E_NEXT, H_V1, s) : -1;
 
-    // stage 6: fresh records
+    // stage 6: fresh records (kernels.py:373-461 restated over the two halves of the bisector)
     if (!split_p) {
         const int32_t a = r4.x;
         p.ids[a] = j << 1;
         p.nexts[a] = right_first;
-        p.prevs[a] = piece_of(cx, tt, E_TWIN, H_V0, s);
-        p.twins[a] = piece_of(cx, tp, E_PREV, H_WHOLE, s);
+        p.prevs[a] = t_v0;
+        p.twins[a] = p_a;
     } else {
         const int32_t a = r4.x, b = r4.y;
         p.ids[a] = j << 2;
-        p.twins[a] = piece_of(cx, tt, E_TWIN, H_V0, s);
+        p.twins[a] = t_v0;
         p.nexts[a] = b;
-        p.prevs[a] = piece_of(cx, tp, E_PREV, H_V0, s);
+        p.prevs[a] = p_a;
         p.ids[b] = (j << 2) + 1;
         p.twins[b] = right_first;
         p.prevs[b] = a;
-        p.nexts[b] = piece_of(cx, tp, E_PREV, H_V2, s);
+        p.nexts[b] = p_b;
     }
     if (!split_n) {
         const int32_t c = right_first;
         p.ids[c] = (j << 1) + 1;
         p.prevs[c] = left_last;
-        p.nexts[c] = piece_of(cx, tt, E_TWIN, H_V1, s);
-        p.twins[c] = piece_of(cx, tn, E_NEXT, H_WHOLE, s);
+        p.nexts[c] = t_v1;
+        p.twins[c] = n_a;
     } else {
         const int32_t c = right_first, d = right_second;
         p.ids[c] = (j << 2) + 2;
         p.twins[c] = left_last;
         p.nexts[c] = d;
-        p.prevs[c] = piece_of(cx, tn, E_NEXT, H_V2, s);
+        p.prevs[c] = n_a;
         p.ids[d] = (j << 2) + 3;
         p.prevs[d] = c;
-        p.twins[d] = piece_of(cx, tt, E_TWIN, H_V1, s);
-        p.nexts[d] = piece_of(cx, tn, E_NEXT, H_V1, s);
+        p.twins[d] = t_v1;
+        p.nexts[d] = n_b;
     }
 
     // stage 7: surviving neighbours across unsplit edges (kernels.py:547-561)
@@ -1248,15 +1272,17 @@ __device__ __forceinline__ void apply_split(ApplyCtx &cx, int32_t s, uint32_t sm
     if (split_p && split_n) set_live(bits32, r4.w);
 }
 
-// one sibling pair (even id e, odd id o) collapses into parent slot par
-__device__ __forceinline__ void apply_merged_pair(ApplyCtx &cx, int32_t e, int32_t o, uint64_t id_e,
-                                                  int32_t par, int32_t twin_slot)
+// one sibling pair (even id e, odd id o) collapses into parent slot par; n_ext / q_ext are the
+// (resolved) bundles of the neighbours across the odd member's twin edge and the even member's
+// twin edge (kernels.py:464-491, 562-594)
+__device__ __forceinline__ void apply_merged_pair(ApplyCtx &cx, int32_t e, int32_t o, uint64_t id_e, int32_t par,
+                                                  int32_t twin_slot, const Neighbour &n_ext, const Neighbour &q_ext)
 {
     const cbtm_pool &p = cx.p;
-    const Neighbour n_ext = load_neighbour(cx, p.twins[o]), q_ext = load_neighbour(cx, p.twins[e]);
+    const int32_t nx = piece_of(cx, n_ext, E_NEXT, H_WHOLE, o), pv = piece_of(cx, q_ext, E_PREV, H_WHOLE, e);
     p.ids[par] = id_e >> 1;
-    p.nexts[par] = piece_of(cx, n_ext, E_NEXT, H_WHOLE, o);
-    p.prevs[par] = piece_of(cx, q_ext, E_PREV, H_WHOLE, e);
+    p.nexts[par] = nx;
+    p.prevs[par] = pv;
     p.twins[par] = twin_slot;
     if (n_ext.slot >= 0 && survives(n_ext)) redirect_to(p, n_ext, o, par, E_PREV);
     if (q_ext.slot >= 0 && survives(q_ext)) redirect_to(p, q_ext, e, par, E_NEXT);
@@ -1283,6 +1309,8 @@ __device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t n, uint
         const int32_t j4_hint = a.ws.j4s[i];
         const uint32_t cmd = p.commands[s];
         const int32_t mref = a.ws.merge_ref[s];
+        OwnRecord own = {};
+        if (na) own = load_own(p, s);
         const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
         if (na == 0) {
             // not allocating: either untouched, or a non-owner member of an agreed merge
@@ -1292,7 +1320,6 @@ __device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t n, uint
             }
             continue;
         }
-        const OwnRecord own = load_own(p, s);
         if (sm) {
             apply_split(cx, s, sm, own);
             ++split_freed;
@@ -1302,23 +1329,43 @@ __device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t n, uint
             ++merge_freed;
             const uint64_t js = own.id;
             const MergeCfg c = merge_config_admitted(js, own.nx, own.pv, cmd, j4_hint);
-            const bool s_even = !(js & 1);
-            const int32_t p1 = own.res.x;
+            const bool quad = c.kind == 2;
+            // round trip: ids and twin pointers of the other members (parities are not known yet, so
+            // everything that may be needed is fetched); round trip: the four outer neighbours'
+            // bundles; round trip: their parents if they merge away; then the stores
             const uint64_t id_sib = p.ids[c.sib];
+            const int32_t tw_sib = p.twins[c.sib];
+            uint64_t jo = 0, id_j4 = 0;
+            int32_t tw_oth = -1, tw_j4 = -1;
+            if (quad) {
+                jo = p.ids[c.oth];
+                id_j4 = p.ids[c.j4];
+                tw_oth = p.twins[c.oth];
+                tw_j4 = p.twins[c.j4];
+            }
+            const bool s_even = !(js & 1), oth_even = !(jo & 1);
+            const int32_t e1 = s_even ? s : c.sib, o1 = s_even ? c.sib : s;
+            const int32_t e2 = oth_even ? c.oth : c.j4, o2 = oth_even ? c.j4 : c.oth;
+            Neighbour n1 = load_neighbour(cx, s_even ? tw_sib : own.tw); // across twins[o1]
+            Neighbour q1 = load_neighbour(cx, s_even ? own.tw : tw_sib); // across twins[e1]
+            Neighbour n2 = load_neighbour(cx, quad ? (oth_even ? tw_j4 : tw_oth) : -1);
+            Neighbour q2 = load_neighbour(cx, quad ? (oth_even ? tw_oth : tw_j4) : -1);
+            resolve_parent(cx, n1);
+            resolve_parent(cx, q1);
+            resolve_parent(cx, n2);
+            resolve_parent(cx, q2);
+            const int32_t p1 = own.res.x;
             const uint64_t id_e1 = s_even ? js : id_sib;
-            if (c.kind == 2) {
+            if (quad) {
                 const int32_t p2 = own.res.y;
-                const uint64_t jo = p.ids[c.oth];
-                const uint64_t id_j4 = p.ids[c.j4];
-                const bool oth_even = !(jo & 1);
                 const uint64_t id_e2 = oth_even ? jo : id_j4;
-                apply_merged_pair(cx, s_even ? s : c.sib, s_even ? c.sib : s, id_e1, p1, p2);
-                apply_merged_pair(cx, oth_even ? c.oth : c.j4, oth_even ? c.j4 : c.oth, id_e2, p2, p1);
+                apply_merged_pair(cx, e1, o1, id_e1, p1, p2, n1, q1);
+                apply_merged_pair(cx, e2, o2, id_e2, p2, p1, n2, q2);
                 set_live(bits32, p1);
                 set_live(bits32, p2);
                 merge_alloc += 2;
             } else {
-                apply_merged_pair(cx, s_even ? s : c.sib, s_even ? c.sib : s, id_e1, p1, -1);
+                apply_merged_pair(cx, e1, o1, id_e1, p1, -1, n1, q1);
                 set_live(bits32, p1);
                 merge_alloc += 1;
             }
