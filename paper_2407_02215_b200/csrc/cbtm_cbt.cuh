@@ -568,6 +568,8 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
             const uint32_t b = gwarp + (k0 + src) * nwarps;
             const uint32_t cnt = __shfl_sync(FULL_MASK, my_cnt, src);
 
+            // the block's bits travel together with the root path (one round trip, not two)
+            const uint32_t own_full = (g.span == 1024u && cnt != 0 && cnt != g.span) ? bits32[(size_t)b * 32 + lane] : 0u;
             // ones before this block: left siblings along the root path
             uint32_t part = 0;
             if (lane >= 1 && lane <= g.lc) {
@@ -593,7 +595,7 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
             const uint32_t z0 = zline + (zeros_before & 31u);
             uint32_t p1 = o1, p0 = z0;
             if (g.span == 1024u) { // every word fully valid (all pools with D >= 10)
-                const uint32_t own = bits32[(size_t)b * 32 + lane];
+                const uint32_t own = own_full;
 #pragma unroll 8
                 for (int w = 0; w < 32; ++w) {
                     const uint32_t word = __shfl_sync(FULL_MASK, own, w);
