@@ -534,6 +534,10 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
             a.ws.need8[i] = (uint8_t)need;
             a.ws.mbits8[i] = (uint8_t)mbits;
         }
+#ifdef CBTM_DEBUG_TIMING
+        __syncthreads();
+        WORK_END(ctl, 0);
+#endif
         uint32_t sum = warp_sum(need);
         if (fast) {
             // one fire-and-forget atomic per warp: warps-done count above, needs below
@@ -1460,7 +1464,6 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
                         reinterpret_cast<int32_t(*)[IDX_STAGE_WORDS]>(dyn_smem), bid, nb);
         else
             phase_reset(a, bid, nb);
-        WORK_END(ctl, 0);
         grid.sync();
         if (stamp) stamp[1] = global_ns();
         const uint32_t n = p.counters[1];      // the frame's live count: one read per CTA, kept in a register
