@@ -120,20 +120,6 @@ int fill_args(const cbtm_pool *pool, const cbtm_verdict *v, FrameArgs *a)
     return 0;
 }
 
-// Co-resident grid for a kernel of CHUNK threads: the look-back scans of the frame
-// phases wait on other CTAs, so no CTA may be left waiting for an SM.
-template <typename K>
-unsigned resident_grid(K kernel, int depth, int cap_per_sm, size_t dyn_smem)
-{
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, CHUNK, dyn_smem) != cudaSuccess || per_sm < 1)
-        per_sm = 1;
-    if (per_sm > cap_per_sm) per_sm = cap_per_sm;
-    const uint64_t want = (((uint64_t)1 << depth) + CHUNK - 1) / CHUNK; // tiny pools: fewer CTAs
-    const uint64_t cap = (uint64_t)sm_count() * per_sm;
-    return (unsigned)(want < cap ? want : cap);
-}
-
 unsigned frame_grid(int depth)
 {
     return strided_grid((uint64_t)1 << depth, CHUNK, 8);
@@ -170,7 +156,7 @@ int finish_staged(const FrameArgs &a, int64_t *stats_seq, bool with_reset, cudaS
 {
     const int d = a.pool.depth;
     if (with_reset) k_reset<<<frame_grid(d), CHUNK, 0, st>>>(a);
-    k_classify_frame<<<resident_grid(k_classify_frame, d, 2, 0), CHUNK, 0, st>>>(a);
+    k_classify_frame<<<frame_grid(d), CHUNK, 0, st>>>(a);
     k_admit<<<1, CHUNK, 0, st>>>(a);
     k_scatter<<<frame_grid(d), CHUNK, 0, st>>>(a);
     k_agree<<<frame_grid(d), CHUNK, 0, st>>>(a);

@@ -571,22 +571,18 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
 
 }
 
-// Fast path, admin CTA: T = total need once every chunk has reported (waits for
-// the other CTAs' chunks, so a CTA with chunks of several pools calls it only
-// after all of them), then the window table.
+// Fast path totals, one CTA, behind the barrier that ends P2 (every chunk's atomic has landed):
+// T = total need, and the other per-frame fields the slow path's phase_admit would have set.
 __device__ __forceinline__ void phase_classify_admin(const FrameArgs &a, uint32_t n)
 {
-    __shared__ unsigned long long s_total;
     const cbtm_pool &p = a.pool;
     Control *ctl = a.ws.ctl;
     if (!fits_a_priori(p, n)) return;
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
     if (threadIdx.x == 0) {
-        unsigned long long v;
-        do asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&ctl->need_total) : "memory");
-        while ((v >> NEED_TOTAL_SHIFT) < (unsigned long long)nch * (CHUNK / 32));
+        const unsigned long long v = ctl->need_total;
         const unsigned long long total = v & ((1ull << NEED_TOTAL_SHIFT) - 1);
-        s_total = total;
+        (void)nch; // (v >> NEED_TOTAL_SHIFT) == nch * (CHUNK / 32): every warp of every chunk has reported
         ctl->need_total = 0; // nobody adds any more this frame
         ctl->n = n;
         ctl->F = (int64_t)(((uint64_t)1 << p.depth) - n);
@@ -596,8 +592,7 @@ __device__ __forceinline__ void phase_classify_admin(const FrameArgs &a, uint32_
         ctl->stats[CBTM_STAT_LIVE_BEFORE] = n;
         ctl->stats[CBTM_STAT_RESERVED] = (int64_t)total;
     }
-    __syncthreads();
-    build_window_table(a, (long long)s_total);
+    __syncthreads(); // ctl->T is read right away by the same CTA (window table)
 }
 
 // ---------------------------------------------------------------------------
@@ -657,8 +652,6 @@ __device__ __forceinline__ void phase_admit(const FrameArgs &a)
             ctl->stats[CBTM_STAT_LIVE_BEFORE] = n;
             ctl->stats[CBTM_STAT_RESERVED] = (int64_t)total_need;
         }
-        __syncthreads();
-        build_window_table(a, (long long)total_need);
         return;
     }
 
@@ -747,8 +740,6 @@ __device__ __forceinline__ void phase_admit(const FrameArgs &a)
         ctl->stats[CBTM_STAT_LIVE_BEFORE] = n;
         ctl->stats[CBTM_STAT_RESERVED] = T;
     }
-    __syncthreads();
-    build_window_table(a, T);
 }
 
 // P2c: scatter the admitted commands (pressure path)
@@ -1395,13 +1386,9 @@ __global__ void __launch_bounds__(CHUNK) k_reset(const __grid_constant__ FrameAr
     phase_reset(a, blockIdx.x, gridDim.x);
 }
 
-// fast path: the admin CTA waits for the other CTAs of the grid, which therefore
-// must all be resident (the host sizes this grid from the kernel's occupancy)
 __global__ void __launch_bounds__(CHUNK) k_classify_frame(const __grid_constant__ FrameArgs a)
 {
-    const uint32_t n = a.pool.counters[1];
-    phase_classify(a, n, blockIdx.x, gridDim.x);
-    if (blockIdx.x == gridDim.x - 1) phase_classify_admin(a, n);
+    phase_classify(a, a.pool.counters[1], blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(CHUNK) k_admit(const __grid_constant__ FrameArgs a)
@@ -1411,12 +1398,18 @@ __global__ void __launch_bounds__(CHUNK) k_admit(const __grid_constant__ FrameAr
 
 __global__ void __launch_bounds__(CHUNK) k_scatter(const __grid_constant__ FrameArgs a)
 {
-    if (!fits_a_priori(a.pool, (uint32_t)a.ws.ctl->n)) phase_scatter(a, blockIdx.x, gridDim.x);
+    if (!fits_a_priori(a.pool, a.pool.counters[1])) phase_scatter(a, blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(CHUNK) k_agree(const __grid_constant__ FrameArgs a)
 {
-    phase_agree(a, (uint32_t)a.ws.ctl->n, blockIdx.x, gridDim.x);
+    // n from the CBT root: ctl->n is only written below (fast path) / by k_admit (slow path)
+    const uint32_t n = a.pool.counters[1];
+    if (blockIdx.x == gridDim.x - 1) {
+        phase_classify_admin(a, n);
+        build_window_table(a, a.ws.ctl->T);
+    }
+    phase_agree(a, n, blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(CHUNK) k_reserve(const __grid_constant__ FrameArgs a)
@@ -1469,7 +1462,6 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         const uint32_t n = p.counters[1];      // the frame's live count: one read per CTA, kept in a register
         const bool fast = fits_a_priori(p, n); // grid-uniform
         phase_classify(a, n, bid, nb);
-        if (bid == nb - 1) phase_classify_admin(a, n);
         WORK_END(ctl, 1);
         grid.sync();
         if (!fast) { // pool under reservation pressure: one CTA admits, then everybody scatters
@@ -1479,6 +1471,12 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
             grid.sync();
         }
         if (stamp) stamp[2] = global_ns();
+        // T is final: the free-rank window table is built by the CTA with the fewest chunks while the
+        // others take the agreement snapshot (it was the straggler of P2 when built there)
+        if (bid == nb - 1) {
+            phase_classify_admin(a, n); // no-op on the slow path (phase_admit did it)
+            build_window_table(a, ctl->T);
+        }
         phase_agree(a, n, bid, nb);
         WORK_END(ctl, 2);
         grid.sync();
@@ -1566,18 +1564,13 @@ k_frames_batch(const __grid_constant__ BatchArgs b, int n_pools, int n_frames)
             phase_classify(b.a[q], b.a[q].pool.counters[1], vbid(q), nb);
             __syncthreads();
         }
-        for (int q = 0; q < n_pools; ++q) // admin duties last: they wait for the other CTAs' chunks
-            if (vbid(q) == nb - 1) {
-                phase_classify_admin(b.a[q], b.a[q].pool.counters[1]);
-                __syncthreads();
-            }
         grid.sync();
         if (any_slow) { // pools under reservation pressure: one CTA each admits, then everybody scatters
             for (int q = 0; q < n_pools; ++q)
                 if (vbid(q) == 0 && !fits_a_priori(b.a[q].pool, b.a[q].pool.counters[1])) phase_admit<CHUNK>(b.a[q]);
             grid.sync();
             for (int q = 0; q < n_pools; ++q)
-                if (!fits_a_priori(b.a[q].pool, (uint32_t)b.a[q].ws.ctl->n)) {
+                if (!fits_a_priori(b.a[q].pool, b.a[q].pool.counters[1])) {
                     phase_scatter(b.a[q], vbid(q), nb);
                     __syncthreads();
                 }
@@ -1585,7 +1578,12 @@ k_frames_batch(const __grid_constant__ BatchArgs b, int n_pools, int n_frames)
         }
         stamp(f, 2);
         for (int q = 0; q < n_pools; ++q) {
-            phase_agree(b.a[q], (uint32_t)b.a[q].ws.ctl->n, vbid(q), nb);
+            const uint32_t nq = b.a[q].pool.counters[1];
+            if (vbid(q) == nb - 1) {
+                phase_classify_admin(b.a[q], nq);
+                build_window_table(b.a[q], b.a[q].ws.ctl->T);
+            }
+            phase_agree(b.a[q], nq, vbid(q), nb);
             __syncthreads();
         }
         grid.sync();
