@@ -30,4 +30,6 @@ print(f"{'phase':26s} {'total us':>9s} {'latest work end us':>19s} {'barrier + s
 for k, name in enumerate(_lib.PHASE_NAMES):
     tot, work = rows[:, 16 + k].mean() / 1e3, rows[:, 22 + k].mean() / 1e3
     print(f"{name:26s} {tot:9.2f} {work:19.2f} {tot - work:18.2f}")
+for k, name in enumerate(("reserve: latest CTA enters", "reserve: window block found", "reserve: slots expanded")):
+    print(f"{name:26s} {'':9s} {rows[:, 28 + k].mean() / 1e3:19.2f}")
 print(f"{'frame':26s} {rows[:, 16:22].sum(axis=1).mean() / 1e3:9.2f}")

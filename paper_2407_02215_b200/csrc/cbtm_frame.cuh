@@ -80,7 +80,7 @@ struct Control {
     unsigned long long phase_t[2][CBTM_STAT_PHASES + 1]; // %globaltimer at the start of each phase, by frame parity
     int64_t stats[CBTM_STATS_WORDS];
 #ifdef CBTM_DEBUG_TIMING
-    unsigned long long work_end[CBTM_STAT_PHASES]; // latest end of a CTA's work in each phase (before the barrier)
+    unsigned long long work_end[CBTM_STAT_PHASES + 3]; // latest end of a CTA's work in each phase (before the barrier); 3 spare probes
 #endif
 };
 
@@ -898,6 +898,7 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, ui
     const uint32_t *win = a.ws.win_prefix;
     const uint32_t *bits32 = reinterpret_cast<const uint32_t *>(p.bits);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    WORK_END(ctl, 6); // (debug) latest CTA entering the phase = barrier exit skew
     const uint32_t win_n = ctl->win_n, win_lo = ctl->win_lo; // CTA-uniform: written before the last barrier
     const uint32_t win_first = win[0]; // (garbage while win_n == 0, never used then)
 
@@ -934,26 +935,46 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, ui
                 if (__syncthreads_or(hit) || top <= (uint32_t)CHUNK) break;
                 top -= CHUNK;
             }
-            for (uint32_t j = s_j0 + warp; j < win_n; j += CHUNK / 32) {
-                const uint32_t first = win[j]; // free rank of the block's first free slot
-                if (first >= hi_rank) break;
+            WORK_END(ctl, 7); // window block found
+            // The interval may span many leaf blocks when the pool is dense around it (few free slots per
+            // block): a warp per block, and the next block's table entry and bits are fetched while the
+            // current one is expanded (one round trip per block otherwise).
+            const uint32_t valid = g.span >= 1024 ? 32u
+                                 : (lane * 32u >= g.span ? 0u : (g.span - lane * 32u >= 32u ? 32u : g.span - lane * 32u));
+            const uint32_t vmask = valid == 32 ? 0xffffffffu : (valid ? (1u << valid) - 1u : 0u);
+            auto fetch = [&](uint32_t j, uint32_t &first, uint32_t &word) {
+                first = 0xffffffffu; // beyond the table: ends the loop
+                word = 0;
+                if (j < win_n) {
+                    first = win[j]; // free rank of the block's first free slot
+                    word = valid ? bits32[(size_t)(win_lo + j) * 32 + lane] : 0xffffffffu;
+                }
+            };
+            uint32_t first, word, first_nx, word_nx;
+            fetch(s_j0 + warp, first, word);
+            for (uint32_t j = s_j0 + warp; first < hi_rank; j += CHUNK / 32) {
+                fetch(j + CHUNK / 32, first_nx, word_nx);
                 const uint32_t b = win_lo + j;
-                const uint32_t valid = g.span >= 1024 ? 32u
-                                     : (lane * 32u >= g.span ? 0u : (g.span - lane * 32u >= 32u ? 32u : g.span - lane * 32u));
-                const uint32_t vmask = valid == 32 ? 0xffffffffu : (valid ? (1u << valid) - 1u : 0u);
-                uint32_t z = valid ? (~bits32[(size_t)b * 32 + lane] & vmask) : 0u;
+                uint32_t z = ~word & vmask;
                 const uint32_t c = __popc(z);
                 uint32_t r = first + warp_inclusive_scan(c) - c; // free rank of this lane's first free slot
                 const int32_t lane_base = (int32_t)(b * g.span + lane * 32);
-                if (r + c <= lo_rank || r >= hi_rank) z = 0; // none of this word's free slots is wanted
-                while (z) {
-                    const int k = __ffs(z) - 1;
-                    z &= z - 1;
-                    if (r >= lo_rank && r < hi_rank) slots[r - lo_rank] = lane_base + k;
-                    ++r;
+                if (r + c > lo_rank && r < hi_rank) { // some of this word's free slots are wanted
+                    // bit by bit with plain ALU operations (find-first-set sits on the quarter-rate
+                    // unit and made this loop the longest step of the phase)
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) {
+                        if ((z >> k) & 1u) {
+                            if (r >= lo_rank && r < hi_rank) slots[r - lo_rank] = lane_base + k;
+                            ++r;
+                        }
+                    }
                 }
+                first = first_nx;
+                word = word_nx;
             }
             __syncthreads();
+            WORK_END(ctl, 8); // slots expanded
         }
         if (na) {
             for (uint32_t k = 0; k < na; ++k) {
@@ -1502,8 +1523,10 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
                                        ctl->phase_t[f & 1]};
             publish_frame(pub, p.counters[1], threadIdx.x);
 #ifdef CBTM_DEBUG_TIMING
-            if (threadIdx.x < CBTM_STAT_PHASES) {
-                const unsigned long long t0 = ctl->phase_t[f & 1][threadIdx.x], t1 = ctl->work_end[threadIdx.x];
+            if (threadIdx.x < CBTM_STAT_PHASES + 3) {
+                // spare probes 6..8 are reported relative to the start of the reserve phase
+                const unsigned long long t0 = ctl->phase_t[f & 1][threadIdx.x < CBTM_STAT_PHASES ? threadIdx.x : 3],
+                                         t1 = ctl->work_end[threadIdx.x];
                 if (stats_seq) stats_seq[(size_t)CBTM_STATS_WORDS * f + 22 + threadIdx.x] = t1 > t0 ? (int64_t)(t1 - t0) : 0;
                 ctl->work_end[threadIdx.x] = 0;
             }
