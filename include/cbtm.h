@@ -272,6 +272,23 @@ int cbtm_update_finish(const cbtm_pool *pool, const cbtm_verdict *verdict, uintp
  *      update).  Returns 0, or CBTM_E_TIMEOUT after timeout_ns. */
 int cbtm_wait_frame(const int64_t *host_stats, int64_t frame, uint64_t timeout_ns);
 
+/* ---- the frame loop of a real-time client (cmd_animate, cli.py:226-237: one update per camera,
+ *      counters read back every frame) without a kernel launch per frame.  cbtm_update_linger =
+ *      cbtm_update (LOD verdict source only) whose kernel, after publishing the frame, keeps
+ *      polling `mailbox` (pinned host memory mapped into the device's address space, i64[64]) for
+ *      up to linger_ns: if request number `request + 1` is posted in time (cbtm_post_request: the
+ *      23 camera parameters, then the number), it runs that frame too, publishes, and listens
+ *      again -- and so on.  A request that is not picked up in time is never served by that
+ *      kernel, so the caller posts only while it knows the kernel still listens (ParallelEngine
+ *      keeps a margin of half the linger time) and otherwise calls cbtm_update_linger again.
+ *      `request` numbers start at 1 and grow by one per frame across launches.  cbtm_pool.stats
+ *      should be host-mapped memory (cbtm_wait_frame).  Work queued on the same stream waits for
+ *      the kernel to stop listening (at most linger_ns after its last frame). */
+int cbtm_update_linger(const cbtm_pool *pool, const cbtm_verdict *verdict, const int64_t *mailbox,
+                       int64_t request, int64_t linger_ns, uintptr_t stream);
+/* host side: mailbox_host is the HOST address of the same buffer */
+int cbtm_post_request(int64_t *mailbox_host, int64_t request, const double *prm);
+
 /* ---- ParallelEngine.run_epochs / cmd_animate (pipeline.py:324-337,
  *      cli.py:226-231) for LOD sequences: n_frames updates back to back, no host
  *      synchronisation; prm_host is HOST f64[n_frames*23]; stats_out (device

@@ -6,6 +6,7 @@
 //        --shared -Xcompiler -fPIC -o libcbtm.so cbtm.cu
 #include <atomic>
 #include <chrono>
+#include <cstring>
 
 #include "cbtm_frame.cuh"
 #include "cbtm_mesh.cuh"
@@ -189,10 +190,13 @@ unsigned persistent_grid(int depth)
     return (unsigned)(want < cap ? want : cap);
 }
 
-// n_frames full updates (optionally without the index phase) in one cooperative launch
-int frames_launch(FrameArgs &a, int n_frames, int64_t *stats_seq, int do_index, unsigned grid, cudaStream_t st)
+// n_frames full updates (optionally without the index phase) in one cooperative launch; with a
+// mailbox: one update, then the kernel lingers for further requests (cbtm_update_linger)
+int frames_launch(FrameArgs &a, int n_frames, int64_t *stats_seq, int do_index, unsigned grid, cudaStream_t st,
+                  const int64_t *mailbox = nullptr, long long linger_ns = 0, long long next_request = 0)
 {
-    void *args[] = {(void *)&a, (void *)&n_frames, (void *)&stats_seq, (void *)&do_index};
+    void *args[] = {(void *)&a,       (void *)&n_frames,  (void *)&stats_seq,   (void *)&do_index,
+                    (void *)&mailbox, (void *)&linger_ns, (void *)&next_request};
     return status(cudaLaunchCooperativeKernel((const void *)k_frames, dim3(grid), dim3(CHUNK), args,
                                               FRAMES_DYN_SMEM, st));
 }
@@ -467,6 +471,40 @@ int cbtm_wait_frame(const int64_t *host_stats, int64_t frame, uint64_t timeout_n
             return CBTM_E_TIMEOUT;
     }
     std::atomic_thread_fence(std::memory_order_acquire);
+    return 0;
+}
+
+int cbtm_update_linger(const cbtm_pool *pool, const cbtm_verdict *verdict, const int64_t *mailbox, int64_t request,
+                       int64_t linger_ns, uintptr_t stream)
+{
+    int rc = check_pool(pool, true);
+    if (rc) return rc;
+    if (!verdict || !mailbox) return CBTM_E_NULL;
+    if (verdict->mode != CBTM_VERDICT_LOD) return CBTM_E_MODE; // later requests carry camera parameters only
+    if (request < 1 || linger_ns < 0 || linger_ns > 100000000) return CBTM_E_RANGE; // at most 100 ms
+    FrameArgs a;
+    rc = fill_args(pool, verdict, &a);
+    if (rc) return rc;
+    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth);
+    if (!grid) { // no cooperative launch: a plain update, nothing lingers
+        rc = index_launch(pool, true, as_stream(stream));
+        return rc ? rc : finish_staged(a, nullptr, false, as_stream(stream));
+    }
+    rc = status(cudaMemsetAsync(&a.ws.ctl->seq_frame, 0, sizeof(uint32_t), as_stream(stream)));
+    if (rc) return rc;
+    return frames_launch(a, 1, nullptr, 1, grid, as_stream(stream), mailbox, linger_ns, request + 1);
+}
+
+int cbtm_post_request(int64_t *mailbox_host, int64_t request, const double *prm)
+{
+    if (!mailbox_host || !prm) return CBTM_E_NULL;
+    for (int k = 0; k < CBTM_PRM_WORDS; ++k) {
+        int64_t bits;
+        memcpy(&bits, &prm[k], sizeof bits);
+        reinterpret_cast<volatile int64_t *>(mailbox_host)[8 + k] = bits;
+    }
+    std::atomic_thread_fence(std::memory_order_release);
+    reinterpret_cast<volatile int64_t *>(mailbox_host)[0] = request;
     return 0;
 }
 

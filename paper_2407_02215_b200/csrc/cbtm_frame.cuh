@@ -74,6 +74,9 @@ struct Control {
     int32_t tail_count;
     uint32_t seq_frame; // index into prm_seq for sequence runs
     unsigned long long need_total; // fast path: warps done << 40 | sum of their needs (zero between frames)
+    int32_t mb_go;                 // linger mode: 1 = a request arrived in time, run another frame
+    int32_t mb_pad_;
+    double mb_prm[CBTM_PRM_WORDS]; // linger mode: the camera parameters of that request
     int32_t tail_idx[TAIL_MAX];
     uint32_t win_lo; // first leaf block of the free-rank window table
     uint32_t win_n;  // leaf blocks in the window table (0: table not built, descend)
@@ -461,7 +464,8 @@ __device__ __forceinline__ void walk_split_chain(const cbtm_pool &p, int32_t s)
     }
 }
 
-__device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb)
+__device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb,
+                                               const double *prm_row = nullptr)
 {
     __shared__ double prm[CBTM_PRM_WORDS];
     __shared__ uint32_t wsum[CHUNK / 32], wmin[CHUNK / 32];
@@ -477,7 +481,8 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
     double prm_reg = 0.0;
     bool prm_pending = a.vmode == CBTM_VERDICT_LOD;
     if (prm_pending && tid < CBTM_PRM_WORDS)
-        prm_reg = a.use_prm_seq ? a.ws.prm_seq[(size_t)CBTM_PRM_WORDS * ctl->seq_frame + tid] : a.prm[tid];
+        prm_reg = prm_row ? prm_row[tid]
+                          : a.use_prm_seq ? a.ws.prm_seq[(size_t)CBTM_PRM_WORDS * ctl->seq_frame + tid] : a.prm[tid];
 
     for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
         const uint32_t i = chunk * CHUNK + tid;
@@ -1455,7 +1460,8 @@ __global__ void __launch_bounds__(CHUNK) k_publish(const __grid_constant__ Frame
 constexpr int FRAMES_DYN_SMEM = IDX_WARPS * IDX_STAGE_WORDS * 4; // 36 KB: index staging
 
 __global__ void __launch_bounds__(CHUNK, 2)
-k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, int do_index)
+k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, int do_index,
+         const volatile int64_t *mailbox, long long linger_ns, long long next_request)
 {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -1469,7 +1475,10 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
     const bool stamper = bid == 0 && threadIdx.x == 0;
     int32_t *free_list = (p.flags & CBTM_POOL_FULL_FREE_CACHE) ? p.cache_free : nullptr;
 
-    for (int f = 0; f < n_frames; ++f) {
+    // linger mode (mailbox != NULL, n_frames == 1): after a frame the kernel polls a host-mapped
+    // mailbox for the next request for up to linger_ns and, if one arrives, runs it without a new
+    // launch (cbtm_update_linger / cbtm_post_request)
+    for (int f = 0; f < n_frames || mailbox; ++f) {
         unsigned long long *stamp = stamper ? ctl->phase_t[f & 1] : nullptr;
         if (stamp) stamp[0] = global_ns();
         if (do_index)
@@ -1482,7 +1491,7 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         if (stamp) stamp[1] = global_ns();
         const uint32_t n = p.counters[1];      // the frame's live count: one read per CTA, kept in a register
         const bool fast = fits_a_priori(p, n); // grid-uniform
-        phase_classify(a, n, bid, nb);
+        phase_classify(a, n, bid, nb, (mailbox && f > 0) ? ctl->mb_prm : nullptr);
         WORK_END(ctl, 1);
         grid.sync();
         if (!fast) { // pool under reservation pressure: one CTA admits, then everybody scatters
@@ -1519,8 +1528,8 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         // the frame's counters go out while the next frame's index phase is already running
         // (pool->stats may be host-mapped memory: only the launch's last frame pays for that write)
         if (bid == nb - 1) {
-            const ReducePublish pub = {ctl->stats, f == n_frames - 1 ? p.stats : nullptr, stats_seq, &ctl->seq_frame,
-                                       ctl->phase_t[f & 1]};
+            const ReducePublish pub = {ctl->stats, (mailbox || f == n_frames - 1) ? p.stats : nullptr, stats_seq,
+                                       &ctl->seq_frame, ctl->phase_t[f & 1]};
             publish_frame(pub, p.counters[1], threadIdx.x);
 #ifdef CBTM_DEBUG_TIMING
             if (threadIdx.x < CBTM_STAT_PHASES + 3) {
@@ -1531,6 +1540,41 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
                 ctl->work_end[threadIdx.x] = 0;
             }
 #endif
+        }
+        if (mailbox) {
+            // One thread watches the mailbox (a load from host memory every ~1.5 us) until request
+            // number next_request + f shows up or the linger time is over; everybody else waits in
+            // the barrier.  The host posts a request only while it knows the kernel is still
+            // listening (ParallelEngine keeps a safety margin) and otherwise launches afresh, so a
+            // request is served exactly once.
+            if (bid == 0 && threadIdx.x < 32) { // one warp: lane 0 watches, then 23 lanes fetch the parameters
+                int go = 0;
+                if (threadIdx.x == 0 && ctl->seq_frame + 1 < (uint32_t)MAX_SEQ_FRAMES) {
+                    const unsigned long long t0 = global_ns();
+                    const long long want = next_request + f;
+                    do {
+                        if (mailbox[0] >= want) {
+                            go = 1;
+                            break;
+                        }
+                    } while (global_ns() - t0 < (unsigned long long)linger_ns);
+                }
+                go = __shfl_sync(FULL_MASK, go, 0);
+                if (go) {
+                    __threadfence_system();
+                    // (one load from host memory per lane, all in flight together: a loop in one
+                    // thread pays a PCIe round trip per word)
+                    if (threadIdx.x < CBTM_PRM_WORDS)
+                        ctl->mb_prm[threadIdx.x] = __longlong_as_double(mailbox[8 + threadIdx.x]);
+                }
+                __syncwarp();
+                if (threadIdx.x == 0) {
+                    ctl->mb_go = go;
+                    __threadfence();
+                }
+            }
+            grid.sync();
+            if (!ctl->mb_go) break; // grid-uniform: rewritten only behind the barriers of another frame
         }
     }
 }

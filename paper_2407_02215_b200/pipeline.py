@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes as C
 import io
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -193,11 +194,21 @@ def evaluate_verdicts(state: TriangulationState, cv, refresh_index: bool = True)
 class ParallelEngine:
     """Executes incremental updates on the GPU that owns the state."""
 
-    def __init__(self, threads: int = 1, profile: bool = False):
+    def __init__(self, threads: int = 1, profile: bool = False, linger_us: float = 0.0):
+        """``linger_us`` > 0 (real-time frame loops): after an update with an LOD
+        verdict source the frame kernel keeps listening on a host-mapped mailbox
+        for that long, and the next update -- if it comes within half of it --
+        is handed over through the mailbox instead of a new kernel launch
+        (cbtm_update_linger / cbtm_post_request: no launch latency, ~15 us per
+        frame).  Other work queued on the state's stream waits until the kernel
+        stops listening."""
         if threads < 1:
             raise ValueError("thread count must be >= 1")
+        if not 0.0 <= linger_us <= 100000.0:
+            raise ValueError("linger_us must lie in [0, 100000]")
         self.threads = threads  # accepted for compatibility; unused on the GPU
         self.profile = profile
+        self.linger_ns = int(linger_us * 1000)
         _lib.load()
 
     def close(self):
@@ -240,7 +251,11 @@ class ParallelEngine:
             events[0].record()
         cv = decide.device_verdict(state) if isinstance(decide, KernelDecide) else None
         keep_alive = None
-        if cv is not None and not events:
+        lingering = False
+        if cv is not None and not events and self.linger_ns and cv.mode == _lib.VERDICT_LOD:
+            lingering = True
+            self._update_linger(state, pool, cv, stream, seq_before)
+        elif cv is not None and not events:
             # device verdict source: stages 1-9 in one call (one cooperative launch)
             _lib.check(L.cbtm_update(C.byref(pool), C.byref(cv), stream), "cbtm_update")
         else:
@@ -259,10 +274,11 @@ class ParallelEngine:
                        "cbtm_update_finish")
             if events:
                 events[2].record()
-        rc = L.cbtm_wait_frame(state._stats_host_ptr, seq_before + 1, 20_000_000_000)
-        if rc:
-            state.synchronize()  # surfaces a CUDA error if the frame kernel died
-            _lib.check(rc, "cbtm_wait_frame")
+        if not lingering:
+            rc = L.cbtm_wait_frame(state._stats_host_ptr, seq_before + 1, 20_000_000_000)
+            if rc:
+                state.synchronize()  # surfaces a CUDA error if the frame kernel died
+                _lib.check(rc, "cbtm_wait_frame")
         words = state._stats_np.tolist()
         if keep_alive is not None or events:
             state.synchronize()
@@ -279,6 +295,44 @@ class ParallelEngine:
                                     + stats.merge_allocs), \
             "live count does not match applied operations"
         return stats
+
+    def _update_linger(self, state, pool, cv, stream, seq_before) -> None:
+        """One LOD frame through the lingering frame kernel: posted to the
+        mailbox while the kernel of the previous update is known to listen,
+        launched otherwise; returns when the frame's counters are on the host."""
+        L = _lib.load()
+        now = time.perf_counter
+        request = state._mb_request + 1
+        state._mb_request = request
+        posted = False
+        if now() < state._mb_listen_until and state._mb_pool is pool:
+            _lib.check(L.cbtm_post_request(state._mb_ptr, request, cv.prm), "cbtm_post_request")
+            posted = True
+        else:
+            _lib.check(L.cbtm_update_linger(C.byref(pool), C.byref(cv), state._mb_ptr, request,
+                                            self.linger_ns, stream), "cbtm_update_linger")
+            state._mb_pool = pool
+        while True:
+            # a posted request is either picked up within the linger time or never
+            timeout = 2 * self.linger_ns + 2_000_000 if posted else 20_000_000_000
+            rc = L.cbtm_wait_frame(state._stats_host_ptr, seq_before + 1, timeout)
+            if rc == 0:
+                break
+            if posted and _lib.torch().cuda.current_stream(state.device).query():
+                # the kernel stopped listening before the request arrived (this thread was
+                # descheduled between the time check and the post): deliver it by a launch
+                if L.cbtm_wait_frame(state._stats_host_ptr, seq_before + 1, 0) == 0:
+                    break
+                _lib.check(L.cbtm_update_linger(C.byref(pool), C.byref(cv), state._mb_ptr, request,
+                                                self.linger_ns, stream), "cbtm_update_linger")
+                state._mb_pool = pool
+                posted = False
+                continue
+            if not posted:
+                state.synchronize()  # surfaces a CUDA error if the frame kernel died
+                _lib.check(rc, "cbtm_wait_frame")
+        # the kernel started listening when it published; half the linger time is the margin
+        state._mb_listen_until = now() + 0.5e-9 * self.linger_ns
 
     def run_epochs(self, state, decide, n: int) -> list[UpdateStats]:
         """n updates; ``decide`` may be an EpochFactory re-bound per epoch."""

@@ -91,6 +91,13 @@ class TriangulationState:
         self.d_stats = t.zeros(_lib.STATS_WORDS, dtype=t.int64).pin_memory()
         self._stats_np = self.d_stats.numpy()
         self._stats_host_ptr = int(self.d_stats.data_ptr())
+        # mailbox of the lingering frame kernel (ParallelEngine(linger_us=...)): request number in
+        # word 0, camera parameters in words 8..30; pinned and device-mapped like the stats
+        self._mb = t.zeros(64, dtype=t.int64).pin_memory()
+        self._mb_ptr = int(self._mb.data_ptr())
+        self._mb_request = 0
+        self._mb_listen_until = 0.0
+        self._mb_pool = None
         self.d_dispatch = t.zeros(4, dtype=t.int32, device=dev)
         self.d_workspace = t.zeros(L.cbtm_workspace_bytes(depth), dtype=t.uint8, device=dev)
         # mesh operators used by the classifier (uploaded once)

@@ -92,6 +92,12 @@ def test_new_entry_points_check_their_arguments(lib):
     assert lib.cbtm_mesh_workspace_bytes(0) == 0 and lib.cbtm_mesh_workspace_bytes(240) > 0
     assert lib.cbtm_mesh_from_polygons(*([None] * 2), 1, 3, 3, *([None] * 8), 0, 0) == 2
     assert lib.cbtm_export_live_triangles(None, None, None, 0, None, 0) == 2
+    assert lib.cbtm_update_linger(None, None, None, 1, 1000, 0) == 2
+    assert lib.cbtm_post_request(None, 1, None) == 2
+    mailbox = np.zeros(64, dtype=np.int64)
+    prm = np.arange(23, dtype=np.float64)
+    assert lib.cbtm_post_request(mailbox.ctypes.data, 7, prm.ctypes.data) == 0
+    assert mailbox[0] == 7 and np.array_equal(mailbox[8:31].view(np.float64), prm)
 
 
 def test_batch_api_validates_before_touching_the_gpu():

@@ -208,3 +208,37 @@ def test_more_planets_than_one_launch_takes():
         assert [stats_words(s) for s in want[p]] == [stats_words(s) for s in got[p]], p
         assert np.array_equal(solo[p].to_host()["nodes"], both[p].to_host()["nodes"]), p
         assert np.array_equal(solo[p].ids, both[p].ids), p
+
+
+def test_linger_mode_matches_plain_updates():
+    """ParallelEngine(linger_us=...): frames handed to the listening frame kernel
+    through the host-mapped mailbox (no launch) == one launch per frame.  Covers
+    back-to-back frames (mailbox), a pause longer than the linger time (fresh
+    launch), other stream work in between, and a changed pool parameter."""
+    import time
+    seq = workloads.cube_sphere_flyin(depth=18, frames=40)
+    a = initialize(seq.mesh, 18)
+    b = initialize(seq.mesh, 18)
+    plain = ParallelEngine()
+    fast = ParallelEngine(linger_us=3000.0)
+    want = []
+    for i, cam in enumerate(seq.cameras):    # (not interleaved with the lingering run: work queued on the
+        if i == 30:                           #  same stream would wait for the listening kernel to give up)
+            a.max_depth = 30
+        want.append(plain.update(a, LodDecide(seq.config, cam, seq.mesh), epoch=i))
+    posted = 0
+    for i, cam in enumerate(seq.cameras):
+        if i == 12:
+            time.sleep(0.02)                 # far beyond the linger time: the kernel has gone
+        if i == 20:
+            assert b.count() == want[i].live_before   # stream work (a device->host read) while the kernel listens
+        if i == 30:
+            b.max_depth = 30                 # pool parameter baked into the listening kernel: must relaunch
+        listening = time.perf_counter() < b._mb_listen_until and b._mb_pool is b.c_pool()
+        sb = fast.update(b, LodDecide(seq.config, cam, seq.mesh), epoch=i)
+        posted += listening
+        assert stats_words(want[i]) == stats_words(sb), i
+    assert posted >= 20, f"only {posted} of 40 frames went through the mailbox"
+    ha, hb = a.to_host(), b.to_host()
+    for k in ha:
+        assert np.array_equal(ha[k], hb[k]), k
