@@ -297,6 +297,12 @@ int cbtm_run_lod_sequence(const cbtm_pool *pool, const double *root_tris,
                           const double *prm_host, int32_t n_frames, int64_t *stats_out,
                           uintptr_t stream);
 
+/* ---- ParallelEngine.run_epochs (pipeline.py:324-337) with one verdict source for all epochs
+ *      (KeepAll / SplitAll / MergeAll / UniformSplit, or one LodDecide): n_frames updates in one
+ *      launch, no host synchronisation; stats_out as above. */
+int cbtm_run_epochs(const cbtm_pool *pool, const cbtm_verdict *verdict, int32_t n_frames,
+                    int64_t *stats_out, uintptr_t stream);
+
 /* ---- the same for a BATCH of independent pools (cmd_animate over several planets, BASELINE
  *      config 5): the n_pools <= CBTM_MAX_BATCH pools advance in lockstep inside one cooperative
  *      launch, sharing every grid barrier -- P latency-bound planets cost little more than one.

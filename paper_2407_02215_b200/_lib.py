@@ -95,6 +95,7 @@ SIGNATURES = {
     "cbtm_run_lod_sequence": (C.c_int, [C.POINTER(CPool), _P, _P, C.c_int32, _P, _UP]),
     "cbtm_update_linger": (C.c_int, [C.POINTER(CPool), C.POINTER(CVerdict), _P, _I64, _I64, _UP]),
     "cbtm_post_request": (C.c_int, [_P, _I64, _P]),
+    "cbtm_run_epochs": (C.c_int, [C.POINTER(CPool), C.POINTER(CVerdict), C.c_int32, _P, _UP]),
     "cbtm_wait_frame": (C.c_int, [_P, _I64, C.c_uint64]),
     "cbtm_run_lod_sequence_batch": (C.c_int, [C.POINTER(CPool), C.c_int32, _P, _P, C.c_int32, _P, _UP]),
 }

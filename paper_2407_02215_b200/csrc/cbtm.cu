@@ -474,6 +474,40 @@ int cbtm_wait_frame(const int64_t *host_stats, int64_t frame, uint64_t timeout_n
     return 0;
 }
 
+int cbtm_run_epochs(const cbtm_pool *pool, const cbtm_verdict *verdict, int32_t n_frames, int64_t *stats_out,
+                    uintptr_t stream)
+{
+    int rc = check_pool(pool, true);
+    if (rc) return rc;
+    if (!verdict) return CBTM_E_NULL;
+    if (verdict->mode == CBTM_VERDICT_EXPLICIT) return CBTM_E_MODE; // explicit verdicts are per frame
+    if (n_frames < 0) return CBTM_E_RANGE;
+    cudaStream_t st = as_stream(stream);
+    FrameArgs a;
+    rc = fill_args(pool, verdict, &a);
+    if (rc) return rc;
+    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth);
+    for (int32_t done = 0; done < n_frames;) {
+        const int32_t batch = n_frames - done < MAX_SEQ_FRAMES ? n_frames - done : MAX_SEQ_FRAMES;
+        rc = status(cudaMemsetAsync(&a.ws.ctl->seq_frame, 0, sizeof(uint32_t), st));
+        if (rc) return rc;
+        int64_t *so = stats_out ? stats_out + (size_t)CBTM_STATS_WORDS * done : nullptr;
+        if (grid) {
+            rc = frames_launch(a, batch, so, 1, grid, st);
+            if (rc) return rc;
+        } else {
+            for (int32_t f = 0; f < batch; ++f) {
+                rc = index_launch(pool, true, st);
+                if (rc) return rc;
+                rc = finish_staged(a, so, false, st);
+                if (rc) return rc;
+            }
+        }
+        done += batch;
+    }
+    return 0;
+}
+
 int cbtm_update_linger(const cbtm_pool *pool, const cbtm_verdict *verdict, const int64_t *mailbox, int64_t request,
                        int64_t linger_ns, uintptr_t stream)
 {

@@ -338,6 +338,19 @@ class ParallelEngine:
         """n updates; ``decide`` may be an EpochFactory re-bound per epoch."""
         if n < 1:
             raise ValueError("epoch count must be >= 1")
+        cv = None
+        if isinstance(decide, KernelDecide) and not getattr(decide, "per_epoch", False) and not self.profile:
+            cv = decide.device_verdict(state)
+        if cv is not None:
+            # one device verdict source for all epochs: the whole run is one launch (cbtm_run_epochs)
+            t = _lib.torch()
+            d_stats = t.zeros((n, _lib.STATS_WORDS), dtype=t.int64, device=state.device)
+            pool = state.c_pool()
+            _lib.check(_lib.load().cbtm_run_epochs(C.byref(pool), C.byref(cv), n, _lib.ptr(d_stats),
+                                                   state.stream()), "cbtm_run_epochs")
+            rows = _lib.to_host(d_stats)
+            state._touched()
+            return [UpdateStats.from_device_words(rows[e], e) for e in range(n)]
         out = []
         for e in range(n):
             d = decide(e) if getattr(decide, "per_epoch", False) else decide

@@ -93,6 +93,7 @@ def test_new_entry_points_check_their_arguments(lib):
     assert lib.cbtm_mesh_from_polygons(*([None] * 2), 1, 3, 3, *([None] * 8), 0, 0) == 2
     assert lib.cbtm_export_live_triangles(None, None, None, 0, None, 0) == 2
     assert lib.cbtm_update_linger(None, None, None, 1, 1000, 0) == 2
+    assert lib.cbtm_run_epochs(None, None, 1, None, 0) == 2
     assert lib.cbtm_post_request(None, 1, None) == 2
     mailbox = np.zeros(64, dtype=np.int64)
     prm = np.arange(23, dtype=np.float64)

@@ -242,3 +242,21 @@ def test_linger_mode_matches_plain_updates():
     ha, hb = a.to_host(), b.to_host()
     for k in ha:
         assert np.array_equal(ha[k], hb[k]), k
+
+
+def test_run_epochs_in_one_launch_equals_per_frame_updates():
+    """ParallelEngine.run_epochs with one device verdict source = cbtm_run_epochs (all epochs in one
+    launch) on BASELINE config 1 (quad, 2^16 pool, uniform depth 12: 18 frames, reservation pressure
+    from frame 10 on): same counters and state as one update per epoch, and the golden live counts."""
+    a = initialize(halfedge.single_quad(), 16)
+    b = initialize(halfedge.single_quad(), 16)
+    with ParallelEngine() as eng:
+        per_frame = [eng.update(a, UniformSplit(12), epoch=e) for e in range(18)]
+        one_launch = eng.run_epochs(b, UniformSplit(12), 18)
+    assert [stats_words(s) for s in per_frame] == [stats_words(s) for s in one_launch]
+    assert one_launch[-1].live_after == 16384 and sum(s.splits_rejected_oom for s in one_launch) > 0
+    rec = load_golden("quad_d16_uniform12")
+    assert [s.live_after for s in one_launch] == [f["stats"]["live_after"] for f in rec["frames"]]
+    ha, hb = a.to_host(), b.to_host()
+    for k in ha:
+        assert np.array_equal(ha[k], hb[k]), k
