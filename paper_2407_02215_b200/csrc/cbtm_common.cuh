@@ -123,16 +123,6 @@ __device__ __forceinline__ int bit_length64(uint64_t x) { return 64 - __clzll((l
 // bisector.py:91-97
 __device__ __forceinline__ int depth_of(uint64_t id, int rank) { return bit_length64(id) - 1 - rank; }
 
-// streaming 128-bit load that does not pollute L1
-__device__ __forceinline__ uint4 ld_stream(const uint4 *p)
-{
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
-
 __device__ __forceinline__ int popc128(const uint4 &v)
 {
     return __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);

@@ -167,44 +167,7 @@ struct MergeCfg {
     uint64_t id_sib, id_oth, id_j4; // ids of the members (valid per kind)
 };
 
-// `nx`, `pv`: the bisector's own next/prev (already loaded by the caller).
-// Loads are grouped so that the whole configuration costs two dependent round
-// trips after nx/pv: {ids[sib], ids[oth], next-or-prev[oth]} then ids[j4].
-__device__ __forceinline__ MergeCfg merge_config(const cbtm_pool &p, uint64_t j1, int32_t nx, int32_t pv)
-{
-    MergeCfg c = {0, -1, -1, -1, 0, 0, 0};
-    if (depth_of(j1, p.rank) < 1) return c; // roots never merge
-    const bool odd = j1 & 1;
-    const int32_t sib = odd ? pv : nx;
-    const int32_t oth = odd ? nx : pv;
-    if (sib < 0) return c;
-    const uint64_t js = p.ids[sib];
-    uint64_t jo = 0;
-    int32_t j4 = -1;
-    if (oth >= 0) {
-        jo = p.ids[oth];
-        j4 = odd ? p.nexts[oth] : p.prevs[oth];
-    }
-    if ((js >> 1) != (j1 >> 1)) return c;
-    c.sib = sib;
-    c.id_sib = js;
-    if (oth < 0) {
-        c.kind = 1;
-        return c;
-    }
-    if (bit_length64(jo) != bit_length64(j1)) return c;
-    if (j4 < 0) return c;
-    const uint64_t j4id = p.ids[j4];
-    if ((j4id >> 1) != (jo >> 1)) return c;
-    c.kind = 2;
-    c.oth = oth;
-    c.j4 = j4;
-    c.id_oth = jo;
-    c.id_j4 = j4id;
-    return c;
-}
-
-// The same test on values gathered ahead of time (phase_classify issues these
+// kernels.py:113-134 on values gathered ahead of time (phase_classify issues these
 // loads before the classifier runs so that their latency hides behind it):
 // js = ids[sib], jo = ids[oth], j4 = next-or-prev[oth]; only ids[j4] is still
 // to be fetched, and only for a quad.
@@ -303,37 +266,8 @@ k_classify(const __grid_constant__ FrameArgs a, int8_t *verdict_out)
         verdict_out[i] = (int8_t)verdict_of(a, prm, p.ids[p.cache_live[i]], (uint32_t)i);
 }
 
-// Leaf block holding the free (unset) rank `rank` and the number of free slots
-// before that block.  One warp descends the counter heap five levels per step:
-// the 32 descendants of a node five levels down are contiguous in the heap, so
-// a step is one coalesced load, a warp scan and a ballot (4 round trips for
-// D = 26 instead of 16 dependent loads).
-__device__ __forceinline__ void warp_find_free_block(const uint32_t *counters, const Geo &g, uint32_t rank,
-                                                     uint32_t &block, uint32_t &free_before)
-{
-    const int lane = threadIdx.x & 31;
-    uint32_t idx = 0, before = 0; // node idx of level l
-    int l = 0;
-    while (l < g.lc) {
-        const int s = g.lc - l < 5 ? g.lc - l : 5;
-        const uint32_t fan = 1u << s;
-        const uint32_t child_span = (uint32_t)(g.n >> (l + s));
-        uint32_t z = 0;
-        if ((uint32_t)lane < fan) z = child_span - counters[(1u << (l + s)) + (idx << s) + lane];
-        const uint32_t incl = warp_inclusive_scan(z);
-        const unsigned hit = __ballot_sync(FULL_MASK, (uint32_t)lane < fan && incl > rank);
-        const int child = hit ? __ffs(hit) - 1 : (int)fan - 1;
-        const uint32_t excl = __shfl_sync(FULL_MASK, incl - z, child);
-        rank -= excl;
-        before += excl;
-        idx = (idx << s) + child;
-        l += s;
-    }
-    block = idx;
-    free_before = before;
-}
-
-// Same search by a whole CTA, eight levels per step (the 256 descendants of a
+// Leaf block holding the free (unset) rank `rank` and the number of free slots before that block.
+// A whole CTA descends the counter heap eight levels per step (the 256 descendants of a
 // node eight levels down are contiguous): two round trips for D = 26.
 // scratch: 32 words, out: 2 words of shared memory.
 __device__ __forceinline__ void cta_find_free_block(const uint32_t *counters, const Geo &g, uint32_t rank,
