@@ -27,13 +27,13 @@
 //               case n * (3 * max_depth + 4) fits the free count -- always true
 //               for a pool sized like the paper's -- nothing can be rejected:
 //               chunks scatter their commands right away and the total T is one
-//               fire-and-forget atomic per chunk; the otherwise idle "admin" CTA
-//               waits for the last of them and builds the free-rank window table
-//               while the others are still walking split chains.
+//               fire-and-forget atomic per warp.
 //               Otherwise (pool under reservation pressure): P2b, one CTA scans
 //               the chunk needs, finds the first rejected rank and runs the
 //               first-fit tail; P2c scatters what was admitted.
-//   P3 agree    stage 5a: merge agreement snapshot, allocation count per chunk
+//   P3 agree    stage 5a: merge agreement snapshot, allocation count per chunk;
+//               meanwhile the CTA with the fewest chunks reads T (complete behind
+//               the P2 barrier, nobody spins) and builds the free-rank window table
 //   P4 reserve  stage 5b: every CTA sums the chunk counts before its chunk
 //               (a redundant range sum instead of a single-CTA scan phase) and
 //               hands out the free slots
@@ -41,6 +41,10 @@
 //   P6 reduce   stage 9: marked leaf blocks recount their line, the levels up to
 //               the tile roots are rebuilt, the few levels above receive each
 //               tile's delta by atomics (no last-CTA pass, no fences)
+//
+// Inside a phase every load that does not depend on another is issued before the
+// first result is consumed or stored (a store between two loads serialises them:
+// the compiler must assume aliasing), which is where most of the last 5 us came from.
 //
 // They run either as ONE persistent cooperative kernel (k_frames: phases
 // separated by grid barriers, any number of frames per launch) or as one kernel
