@@ -90,6 +90,8 @@ enum {
     CBTM_STAT_ALLOCATED = 9, /* A: slots actually allocated              */
     CBTM_STAT_POISON = 10,   /* fresh pointers resolved to the poison -2 */
     CBTM_STAT_FRAME = 11,    /* frames applied to this pool so far       */
+    CBTM_STAT_PEAK_DEPTH = 12, /* deepest live bisector at the start of the frame (the per-frame
+                                * reduction cmd_animate does on the host, cli.py:232-237)   */
     CBTM_STAT_SEQ = 31,      /* = CBTM_STAT_FRAME, but stored LAST: the other words are written, then a
                               * system-scope fence, then this one -- so when cbtm_pool.stats points to
                               * host-mapped pinned memory the host may poll this word (cbtm_wait_frame)

@@ -34,7 +34,7 @@ VERDICT_CONST, VERDICT_UNIFORM, VERDICT_LOD, VERDICT_EXPLICIT = 0, 1, 2, 3
 
 STAT_NAMES = ("oom_splits", "oom_merges", "split_freed", "merge_freed",
               "split_alloc", "merge_alloc", "live_before", "live_after",
-              "reserved", "allocated", "poison", "frame")
+              "reserved", "allocated", "poison", "frame", "peak_depth")
 
 _ERRORS = {1: "depth out of range", 2: "required pointer is NULL",
            3: "workspace too small", 4: "unknown verdict mode",

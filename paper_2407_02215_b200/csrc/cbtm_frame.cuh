@@ -447,6 +447,11 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
             }
             gathered = {id, js, jo, sib, oth, j4, nx, pv};
         }
+        { // deepest live bisector of the frame (one reduction + one fire-and-forget atomic per warp)
+            const int d = i < n ? depth_of(gathered.id, p.rank) : 0;
+            const int dmax = __reduce_max_sync(FULL_MASK, d);
+            if (lane == 0 && dmax > 0) atomicMax((long long *)&ctl->stats[CBTM_STAT_PEAK_DEPTH], (long long)dmax);
+        }
         if (prm_pending) { // CTA-uniform
             if (tid < CBTM_PRM_WORDS) prm[tid] = prm_reg;
             __syncthreads();

@@ -50,6 +50,7 @@ class UpdateStats:
     reserved_slots: int = 0   # T: slots reserved by admitted commands
     poison: int = 0           # fresh pointers that resolved to the poison -2
     phase_ns: list = field(default_factory=lambda: [0] * 6)  # device ns per phase (_lib.PHASE_NAMES)
+    peak_depth: int = 0       # deepest live bisector at the start of the frame (cli.py:232-237, on device)
 
     @property
     def structural_ops(self) -> int:
@@ -77,7 +78,7 @@ class UpdateStats:
         else:
             ph = [0] * _N_PHASES
             times = list(times) if times is not None else [0] * 9
-        return cls(epoch, w[6], w[7], w[2], w[3], w[0], w[1], w[4], w[5], times, w[8], w[10], ph)
+        return cls(epoch, w[6], w[7], w[2], w[3], w[0], w[1], w[4], w[5], times, w[8], w[10], ph, w[12])
 
 
 _N_PHASES = len(_lib.PHASE_NAMES)

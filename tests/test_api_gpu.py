@@ -213,3 +213,21 @@ def test_device_validator_reports_corruption():
     assert dev["no_reciprocal"] == sum("no reciprocal" in v for v in host)
     assert dev["depth_gaps"] == sum("depth gap" in v for v in host)
     assert dev["first_bad_slot"] >= 0
+
+
+def test_peak_depth_is_reduced_on_the_device():
+    """UpdateStats.peak_depth = deepest live bisector at the start of the frame -- the per-frame
+    reduction cmd_animate does on the host (cli.py:232-237) -- for single updates and sequences."""
+    from paper_2407_02215_b200 import workloads
+    seq = workloads.cube_sphere_flyin(depth=16, frames=12)
+    st = initialize(seq.mesh, 16)
+    with ParallelEngine() as eng:
+        for i, cam in enumerate(seq.cameras[:6]):
+            want = max(bisector.depth_of(int(b), st.rank) for b in st.ids[st.live_slots()])
+            s = eng.update(st, lod.LodDecide(seq.config, cam, seq.mesh), epoch=i)
+            assert s.peak_depth == want, i
+        before = max(bisector.depth_of(int(b), st.rank) for b in st.ids[st.live_slots()])
+        rows = eng.run_lod_sequence(st, seq.params()[6:])
+        assert rows[0].peak_depth == before
+        after = max(bisector.depth_of(int(b), st.rank) for b in st.ids[st.live_slots()])
+        assert eng.update(st, KeepAll()).peak_depth == after
