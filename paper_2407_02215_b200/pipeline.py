@@ -242,6 +242,8 @@ class ParallelEngine:
         writes them into host-mapped memory; waiting for their sequence word is
         the only synchronisation (no copy, no stream synchronise)."""
         L = _lib.load()
+        # the reference reads cbt.count() first, which asserts a reduced tree (pipeline.py:211, cbt.py:70-73)
+        assert not state.cbt._dirty, "sum_reduce required before count()"
         pool = state.c_pool()
         stream = state.stream()
         seq_before = int(state._stats_np[_lib.STAT_SEQ])
