@@ -28,9 +28,10 @@
 //               for a pool sized like the paper's -- nothing can be rejected:
 //               chunks scatter their commands right away and the total T is one
 //               fire-and-forget atomic per warp.
-//               Otherwise (pool under reservation pressure): P2b, one CTA scans
-//               the chunk needs, finds the first rejected rank and runs the
-//               first-fit tail; P2c scatters what was admitted.
+//               Otherwise the scatter follows behind the barrier: everything, if the
+//               total (known then) fits; under real reservation pressure one CTA
+//               first scans the chunk needs, finds the first rejected rank and
+//               runs the first-fit tail (P2b), then P2c scatters what was admitted.
 //   P3 agree    stage 5a: merge agreement snapshot, allocation count per chunk;
 //               meanwhile the CTA with the fewest chunks reads T (complete behind
 //               the P2 barrier, nobody spins) and builds the free-rank window table
@@ -487,9 +488,9 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
         WORK_END(ctl, 0);
 #endif
         uint32_t sum = warp_sum(need);
+        // the frame's total need: one fire-and-forget atomic per warp (warps-done count above, needs below)
+        if (lane == 0) atomicAdd(&ctl->need_total, (unsigned long long)sum | (1ull << NEED_TOTAL_SHIFT));
         if (fast) {
-            // one fire-and-forget atomic per warp: warps-done count above, needs below
-            if (lane == 0) atomicAdd(&ctl->need_total, (unsigned long long)sum | (1ull << NEED_TOTAL_SHIFT));
             if (need == 2)
                 atomicOr(&p.commands[s], mbits);
             else if (need)
@@ -519,26 +520,32 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
 
 }
 
-// Fast path totals, one CTA, behind the barrier that ends P2 (every chunk's atomic has landed):
-// T = total need, and the other per-frame fields the slow path's phase_admit would have set.
-__device__ __forceinline__ void phase_classify_admin(const FrameArgs &a, uint32_t n)
+// The frame's total need (complete behind the barrier that ends P2) and whether all of it fits.
+// Grid-uniform; need_total is zeroed by frame_totals, behind another barrier.
+__device__ __forceinline__ bool frame_fits(const FrameArgs &a, uint32_t n)
+{
+    const unsigned long long total = a.ws.ctl->need_total & ((1ull << NEED_TOTAL_SHIFT) - 1);
+    return total <= (((unsigned long long)1 << a.pool.depth) - n);
+}
+
+// One CTA, once per frame, after the scatter: if the frame fits, T = total need and the other
+// per-frame fields phase_admit would have set; in any case need_total returns to zero.
+__device__ __forceinline__ void frame_totals(const FrameArgs &a, uint32_t n, bool fits)
 {
     const cbtm_pool &p = a.pool;
     Control *ctl = a.ws.ctl;
-    if (!fits_a_priori(p, n)) return;
-    const uint32_t nch = (n + CHUNK - 1) / CHUNK;
     if (threadIdx.x == 0) {
-        const unsigned long long v = ctl->need_total;
-        const unsigned long long total = v & ((1ull << NEED_TOTAL_SHIFT) - 1);
-        (void)nch; // (v >> NEED_TOTAL_SHIFT) == nch * (CHUNK / 32): every warp of every chunk has reported
-        ctl->need_total = 0; // nobody adds any more this frame
-        ctl->n = n;
-        ctl->F = (int64_t)(((uint64_t)1 << p.depth) - n);
-        ctl->T = (int64_t)total;
-        ctl->i0 = n;
-        ctl->tail_count = 0;
-        ctl->stats[CBTM_STAT_LIVE_BEFORE] = n;
-        ctl->stats[CBTM_STAT_RESERVED] = (int64_t)total;
+        const unsigned long long total = ctl->need_total & ((1ull << NEED_TOTAL_SHIFT) - 1);
+        ctl->need_total = 0;
+        if (fits) {
+            ctl->n = n;
+            ctl->F = (int64_t)(((uint64_t)1 << p.depth) - n);
+            ctl->T = (int64_t)total;
+            ctl->i0 = n;
+            ctl->tail_count = 0;
+            ctl->stats[CBTM_STAT_LIVE_BEFORE] = n;
+            ctl->stats[CBTM_STAT_RESERVED] = (int64_t)total;
+        }
     }
     __syncthreads(); // ctl->T is read right away by the same CTA (window table)
 }
@@ -691,17 +698,19 @@ __device__ __forceinline__ void phase_admit(const FrameArgs &a)
 }
 
 // P2c: scatter the admitted commands (pressure path)
-__device__ __forceinline__ void phase_scatter(const FrameArgs &a, uint32_t bid, uint32_t nb)
+// all_n != 0: every request of the frame's all_n live ranks is admitted (the scan total fits), the
+// admission fields of the control block are not consulted (they are written later)
+__device__ __forceinline__ void phase_scatter(const FrameArgs &a, uint32_t bid, uint32_t nb, uint32_t all_n = 0)
 {
     __shared__ int32_t tail[TAIL_MAX];
     __shared__ uint32_t oom[2];
     const cbtm_pool &p = a.pool;
     const Control *ctl = a.ws.ctl;
     const int tid = threadIdx.x;
-    const uint32_t n = (uint32_t)ctl->n;
+    const uint32_t n = all_n ? all_n : (uint32_t)ctl->n;
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
-    const long long i0 = ctl->i0;
-    const int tail_count = ctl->tail_count;
+    const long long i0 = all_n ? (long long)n : ctl->i0;
+    const int tail_count = all_n ? 0 : ctl->tail_count;
     if (tid < TAIL_MAX) tail[tid] = tid < tail_count ? ctl->tail_idx[tid] : -1;
     if (tid < 2) oom[tid] = 0;
     __syncthreads();
@@ -1362,12 +1371,14 @@ __global__ void __launch_bounds__(CHUNK) k_classify_frame(const __grid_constant_
 
 __global__ void __launch_bounds__(CHUNK) k_admit(const __grid_constant__ FrameArgs a)
 {
-    if (!fits_a_priori(a.pool, a.pool.counters[1])) phase_admit<CHUNK>(a);
+    const uint32_t n = a.pool.counters[1];
+    if (!fits_a_priori(a.pool, n) && !frame_fits(a, n)) phase_admit<CHUNK>(a);
 }
 
 __global__ void __launch_bounds__(CHUNK) k_scatter(const __grid_constant__ FrameArgs a)
 {
-    if (!fits_a_priori(a.pool, a.pool.counters[1])) phase_scatter(a, blockIdx.x, gridDim.x);
+    const uint32_t n = a.pool.counters[1];
+    if (!fits_a_priori(a.pool, n)) phase_scatter(a, blockIdx.x, gridDim.x, frame_fits(a, n) ? n : 0);
 }
 
 __global__ void __launch_bounds__(CHUNK) k_agree(const __grid_constant__ FrameArgs a)
@@ -1375,7 +1386,7 @@ __global__ void __launch_bounds__(CHUNK) k_agree(const __grid_constant__ FrameAr
     // n from the CBT root: ctl->n is only written below (fast path) / by k_admit (slow path)
     const uint32_t n = a.pool.counters[1];
     if (blockIdx.x == gridDim.x - 1) {
-        phase_classify_admin(a, n);
+        frame_totals(a, n, fits_a_priori(a.pool, n) || frame_fits(a, n));
         build_window_table(a, a.ws.ctl->T);
     }
     phase_agree(a, n, blockIdx.x, gridDim.x);
@@ -1437,17 +1448,22 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         phase_classify(a, n, bid, nb, (mailbox && f > 0) ? ctl->mb_prm : nullptr);
         WORK_END(ctl, 1);
         grid.sync();
-        if (!fast) { // pool under reservation pressure: one CTA admits, then everybody scatters
-            if (bid == 0) phase_admit<CHUNK>(a);
-            grid.sync();
-            phase_scatter(a, bid, nb);
+        const bool fits = fast || frame_fits(a, n); // grid-uniform
+        if (!fast) {
+            if (fits) { // the total turned out to fit: everything is admitted, scatter now
+                phase_scatter(a, bid, nb, n);
+            } else { // reservation pressure: one CTA admits (first rejected rank, first-fit tail), then everybody scatters
+                if (bid == 0) phase_admit<CHUNK>(a);
+                grid.sync();
+                phase_scatter(a, bid, nb);
+            }
             grid.sync();
         }
         if (stamp) stamp[2] = global_ns();
         // T is final: the free-rank window table is built by the CTA with the fewest chunks while the
         // others take the agreement snapshot (it was the straggler of P2 when built there)
         if (bid == nb - 1) {
-            phase_classify_admin(a, n); // no-op on the slow path (phase_admit did it)
+            frame_totals(a, n, fits);
             build_window_table(a, ctl->T);
         }
         phase_agree(a, n, bid, nb);
@@ -1568,29 +1584,40 @@ k_frames_batch(const __grid_constant__ BatchArgs b, int n_pools, int n_frames)
         }
         grid.sync();
         stamp(f, 1);
-        bool any_slow = false; // grid-uniform
+        bool any_late = false; // grid-uniform
         for (int q = 0; q < n_pools; ++q) {
-            any_slow |= !fits_a_priori(b.a[q].pool, b.a[q].pool.counters[1]);
+            any_late |= !fits_a_priori(b.a[q].pool, b.a[q].pool.counters[1]);
             phase_classify(b.a[q], b.a[q].pool.counters[1], vbid(q), nb);
             __syncthreads();
         }
         grid.sync();
-        if (any_slow) { // pools under reservation pressure: one CTA each admits, then everybody scatters
-            for (int q = 0; q < n_pools; ++q)
-                if (vbid(q) == 0 && !fits_a_priori(b.a[q].pool, b.a[q].pool.counters[1])) phase_admit<CHUNK>(b.a[q]);
-            grid.sync();
-            for (int q = 0; q < n_pools; ++q)
-                if (!fits_a_priori(b.a[q].pool, b.a[q].pool.counters[1])) {
-                    phase_scatter(b.a[q], vbid(q), nb);
+        // per pool (bit q): 1 = the commands were scattered in P2 or the scan total fits, 0 = pressure
+        unsigned fits_mask = 0;
+        for (int q = 0; q < n_pools; ++q) {
+            const uint32_t nq = b.a[q].pool.counters[1];
+            if (fits_a_priori(b.a[q].pool, nq) || frame_fits(b.a[q], nq)) fits_mask |= 1u << q;
+        }
+        if (any_late) { // pools that could not scatter in P2
+            const bool any_pressure = fits_mask != (1u << n_pools) - 1u;
+            if (any_pressure) { // one CTA each admits (first rejected rank, first-fit tail)
+                for (int q = 0; q < n_pools; ++q)
+                    if (vbid(q) == 0 && !((fits_mask >> q) & 1u)) phase_admit<CHUNK>(b.a[q]);
+                grid.sync();
+            }
+            for (int q = 0; q < n_pools; ++q) {
+                const uint32_t nq = b.a[q].pool.counters[1];
+                if (!fits_a_priori(b.a[q].pool, nq)) {
+                    phase_scatter(b.a[q], vbid(q), nb, ((fits_mask >> q) & 1u) ? nq : 0u);
                     __syncthreads();
                 }
+            }
             grid.sync();
         }
         stamp(f, 2);
         for (int q = 0; q < n_pools; ++q) {
             const uint32_t nq = b.a[q].pool.counters[1];
             if (vbid(q) == nb - 1) {
-                phase_classify_admin(b.a[q], nq);
+                frame_totals(b.a[q], nq, (fits_mask >> q) & 1u);
                 build_window_table(b.a[q], b.a[q].ws.ctl->T);
             }
             phase_agree(b.a[q], nq, vbid(q), nb);
