@@ -96,3 +96,36 @@ def test_config4_cbt_2_28_properties():
     assert np.array_equal(c.one_to_bit_ids(ranks.cpu().numpy()), live[ranks].cpu().numpy())
     zr = torch.randint(0, n - popcount, (1 << 16,), device=dev)
     assert np.array_equal(c.zero_to_bit_ids(zr.cpu().numpy()), free[zr].cpu().numpy())
+
+
+def test_maximum_pool_2_30_equals_2_24_slot_for_slot():
+    """The largest pool the ABI allows (2^30 slots: 56 GB of records + 12 GB of scratch, int32 slot
+    indices and uint32 counters at their limits).  Without reservation pressure every decision of a
+    frame -- admission, free ranks, slot placement -- is independent of how many untouched free slots
+    lie behind the ones in use, so the run must equal the same sequence on a 2^24 pool slot for slot:
+    counters, active list, records at the live slots, and the common prefix of the CBT."""
+    import torch
+    free_bytes, _ = torch.cuda.mem_get_info()
+    if free_bytes < 80 * 2 ** 30:
+        pytest.skip("needs ~70 GB of device memory")
+    seq = workloads.earth_sweep(depth=30, frames=24)
+    prms = seq.params()[:24]
+    big = initialize(seq.mesh, 30)
+    small = initialize(seq.mesh, 24)
+    with ParallelEngine() as eng:
+        rows_big = eng.run_lod_sequence(big, prms)
+        rows_small = eng.run_lod_sequence(small, prms)
+    assert [r.csv_row(no_timing=True) for r in rows_big] == [r.csv_row(no_timing=True) for r in rows_small]
+    assert all(r.poison == 0 for r in rows_big) and rows_big[-1].live_after > 20000
+    n = rows_big[-1].live_before          # the active list both pools hold is the last frame's
+    assert torch.equal(big.d_cache_live[:n], small.d_cache_live[:n])
+    cap = small.capacity
+    for k in ("ids", "nexts", "prevs", "twins", "commands", "reserved"):
+        assert torch.equal(getattr(big, "d_" + k)[:cap], getattr(small, "d_" + k)[:cap]), k
+    assert torch.equal(big.d_bits[:cap // 64], small.d_bits)
+    assert not bool(big.d_bits[cap // 64:].any())                    # nothing beyond the small pool was touched
+    assert int(big.d_counters[1].item()) == int(small.d_counters[1].item()) == rows_big[-1].live_after
+    dev = big.validate_device()
+    assert (dev["bad_ids"], dev["too_deep"], dev["dangling"], dev["no_reciprocal"], dev["depth_gaps"]) == (0,) * 5
+    del big
+    torch.cuda.empty_cache()
