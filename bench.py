@@ -229,10 +229,10 @@ def reduce_roofline(L, _lib, torch, device, d_bits, depth, peak, peak_src):
     copies = 8
     bits = [d_bits.clone() for _ in range(copies)]
     cnts = [torch.zeros(L.cbtm_counter_words(depth), dtype=torch.int32, device=device) for _ in range(copies)]
-    ws = torch.zeros(256, dtype=torch.uint8, device=device)
+    ws = torch.zeros(1024, dtype=torch.uint8, device=device)
 
     def launch(k):
-        rc = L.cbtm_sum_reduce(bits[k].data_ptr(), cnts[k].data_ptr(), depth, ws.data_ptr(), 256, stream)
+        rc = L.cbtm_sum_reduce(bits[k].data_ptr(), cnts[k].data_ptr(), depth, ws.data_ptr(), 1024, stream)
         assert rc == 0
 
     cold_ms = _time_batched(torch, device, flush, launch, copies)
@@ -270,10 +270,10 @@ def config4_probe(L, _lib, torch, device, peak):
     bits = [torch.randint(-2 ** 63, 2 ** 63 - 1, (n // 64,), dtype=torch.int64, device=device, generator=gen)]
     bits += [bits[0].clone() for _ in range(copies - 1)]
     cnts = [torch.zeros(L.cbtm_counter_words(depth), dtype=torch.int32, device=device) for _ in range(copies)]
-    ws = torch.zeros(256, dtype=torch.uint8, device=device)
+    ws = torch.zeros(1024, dtype=torch.uint8, device=device)
 
     def reduce(k):
-        assert L.cbtm_sum_reduce(bits[k].data_ptr(), cnts[k].data_ptr(), depth, ws.data_ptr(), 256, stream) == 0
+        assert L.cbtm_sum_reduce(bits[k].data_ptr(), cnts[k].data_ptr(), depth, ws.data_ptr(), 1024, stream) == 0
 
     red_ms = _time_batched(torch, device, flush, reduce, copies, reps=10)
     ones = int(cnts[0][1].item())

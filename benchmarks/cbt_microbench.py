@@ -108,7 +108,7 @@ def main():
     for depth in args.depths:
         n = 1 << depth
         counters = torch.zeros(L.cbtm_counter_words(depth), dtype=torch.int32, device=dev)
-        ws = torch.zeros(256, dtype=torch.uint8, device=dev)
+        ws = torch.zeros(1024, dtype=torch.uint8, device=dev)
         live = torch.empty(n, dtype=torch.int32, device=dev)
         free = torch.empty(n, dtype=torch.int32, device=dev)
         K = 1 << 20
@@ -122,7 +122,7 @@ def main():
             cnt_k = [counters] + [torch.zeros_like(counters) for _ in range(nb - 1)]
 
             def reduce(k=0):
-                rc = L.cbtm_sum_reduce(bits_k[k].data_ptr(), cnt_k[k].data_ptr(), depth, ws.data_ptr(), 256, stream)
+                rc = L.cbtm_sum_reduce(bits_k[k].data_ptr(), cnt_k[k].data_ptr(), depth, ws.data_ptr(), 1024, stream)
                 assert rc == 0
 
             def index(k=0):

@@ -11,10 +11,10 @@ n = 1 << depth
 gen = torch.Generator(device=dev); gen.manual_seed(depth)
 bits = torch.randint(-2 ** 63, 2 ** 63 - 1, (max(n // 64, 16),), dtype=torch.int64, device=dev, generator=gen)
 cnt = torch.zeros(L.cbtm_counter_words(depth), dtype=torch.int32, device=dev)
-ws = torch.zeros(256, dtype=torch.uint8, device=dev)
+ws = torch.zeros(1024, dtype=torch.uint8, device=dev)
 st = torch.cuda.current_stream(dev).cuda_stream
 for _ in range(3):
-    assert L.cbtm_sum_reduce(bits.data_ptr(), cnt.data_ptr(), depth, ws.data_ptr(), 256, st) == 0
+    assert L.cbtm_sum_reduce(bits.data_ptr(), cnt.data_ptr(), depth, ws.data_ptr(), 1024, st) == 0
 if what == "index":
     live = torch.empty(n, dtype=torch.int32, device=dev)
     free = torch.empty(n, dtype=torch.int32, device=dev)
