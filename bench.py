@@ -105,6 +105,12 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.rows.append([c.strip() for c in line.split(",")])
 
+    def wait_first(self, seconds: float):
+        """Block until nvidia-smi has delivered its first sample (or give up)."""
+        t0 = time.time()
+        while self.proc is not None and not self.rows and time.time() - t0 < seconds:
+            time.sleep(0.01)
+
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -329,6 +335,11 @@ def run_gpu(args):
     seq, down, cycle = sweep_params(args.depth, 45.0 * rank)
     K, W = args.steps, args.warmup
     eng = ParallelEngine()
+    # clocks are sampled from before the setup frames until after the e2e runs: the device-timed
+    # region itself is a few ms, shorter than nvidia-smi's sampling period
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
     state = initialize(seq.mesh, args.depth, device=device, staged_launches=args.staged)
     eng.run_lod_sequence(state, down)                       # setup: fly to the ground
     eng.run_lod_sequence(state, step_params(cycle, 0, W))   # warm-up steps
@@ -346,10 +357,9 @@ def run_gpu(args):
     d_stats = torch.zeros((K, _lib.STATS_WORDS), dtype=torch.int64, device=device)
     pinned = torch.from_numpy(timed_prm).pin_memory()
     pool = state.c_pool()
-    sampler = ClockSampler(local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if rank == 0:
-        sampler.start()
+        sampler.wait_first(2.0)
     barrier()
     ev0.record()
     rc = L.cbtm_run_lod_sequence(C.byref(pool), _lib.ptr(state.d_root_tris), pinned.data_ptr(), K,
@@ -359,7 +369,6 @@ def run_gpu(args):
     _lib.check(rc, "cbtm_run_lod_sequence")
     state._touched()
     gpu_ms = ev0.elapsed_time(ev1)
-    clocks = sampler.stop() if rank == 0 else None
     rows = d_stats.cpu().numpy()
     units = int(rows[:, 6].sum())
 
@@ -386,6 +395,7 @@ def run_gpu(args):
     e2e_s = e2e_run(linger_eng, e2e_state2) if args.linger_us > 0 else e2e_launch_s
     if args.linger_us > 0:
         e2e_s -= args.linger_us * 1e-6  # the final kernel's idle listening after the last frame is not frame time
+    clocks = sampler.stop() if rank == 0 else None
     for other in ((e2e_state, e2e_state2) if args.linger_us > 0 else (e2e_state,)):
         same = all(torch.equal(getattr(state, "d_" + k), getattr(other, "d_" + k))
                    for k in ("ids", "nexts", "prevs", "twins", "commands", "reserved", "bits", "counters"))
