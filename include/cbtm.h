@@ -71,6 +71,9 @@ extern "C" {
                                           bit per slot) instead of through the window table -- the path
                                           taken automatically when a frame's allocations span more than
                                           4096 leaf blocks; the flag exists so that tests can exercise it */
+#define CBTM_POOL_WIDE_GRID 8u /* persistent frame kernel with 4 instead of 2 CTAs per SM: pays off from
+                                 ~10^5 live bisectors on (each CTA then works through several chunks of
+                                 256 ranks per phase); same results */
 #define CBTM_POOL_STAGED_LAUNCHES 2u /* one kernel launch per pipeline stage instead of
                                         the persistent cooperative frame kernel (per-stage
                                         profiling; automatic where cooperative launch is

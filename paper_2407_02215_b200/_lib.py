@@ -29,6 +29,7 @@ MAX_BATCH = 8
 POOL_FULL_FREE_CACHE = 1
 POOL_STAGED_LAUNCHES = 2
 POOL_DESCEND_FREE_RANKS = 4
+POOL_WIDE_GRID = 8
 
 VERDICT_CONST, VERDICT_UNIFORM, VERDICT_LOD, VERDICT_EXPLICIT = 0, 1, 2, 3
 

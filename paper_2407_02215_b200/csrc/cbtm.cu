@@ -168,27 +168,31 @@ int finish_staged(const FrameArgs &a, int64_t *stats_seq, bool with_reset, cudaS
     return upper_reduce_launch(a, stats_seq, st);
 }
 
-// Co-resident grid of the persistent frame kernel (0: cooperative launch unavailable)
-unsigned persistent_grid(int depth)
+// Co-resident grid of the persistent frame kernel (0: cooperative launch unavailable); wide = 4 CTAs per SM
+unsigned persistent_grid(int depth, bool wide = false)
 {
-    static int ctas_per_sm = -1;
-    if (ctas_per_sm < 0) {
+    static int ctas_per_sm[2] = {-1, -1};
+    int &cached = ctas_per_sm[wide ? 1 : 0];
+    if (cached < 0) {
+        const void *kernel = wide ? (const void *)k_frames<4> : (const void *)k_frames<2>;
+        const int want_per_sm = wide ? 4 : 2;
         int dev = 0, coop = 0, per_sm = 0;
-        ctas_per_sm = 0;
+        cached = 0;
         if (cudaGetDevice(&dev) == cudaSuccess &&
             cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) == cudaSuccess && coop &&
-            cudaFuncSetAttribute(k_frames, cudaFuncAttributeMaxDynamicSharedMemorySize, FRAMES_DYN_SMEM) ==
+            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FRAMES_DYN_SMEM) ==
                 cudaSuccess &&
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_frames, CHUNK, FRAMES_DYN_SMEM) ==
-                cudaSuccess)
-            ctas_per_sm = per_sm > 2 ? 2 : per_sm;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, CHUNK, FRAMES_DYN_SMEM) == cudaSuccess)
+            cached = per_sm > want_per_sm ? want_per_sm : per_sm;
         (void)cudaGetLastError();
     }
-    if (ctas_per_sm <= 0) return 0;
+    if (cached <= 0) return 0;
     const uint64_t want = (((uint64_t)1 << depth) + CHUNK - 1) / CHUNK; // tiny pools: fewer CTAs, cheaper barriers
-    const uint64_t cap = (uint64_t)sm_count() * ctas_per_sm;
+    const uint64_t cap = (uint64_t)sm_count() * cached;
     return (unsigned)(want < cap ? want : cap);
 }
+
+inline bool wide(const cbtm_pool *pool) { return (pool->flags & CBTM_POOL_WIDE_GRID) != 0; }
 
 // n_frames full updates (optionally without the index phase) in one cooperative launch; with a
 // mailbox: one update, then the kernel lingers for further requests (cbtm_update_linger)
@@ -197,8 +201,8 @@ int frames_launch(FrameArgs &a, int n_frames, int64_t *stats_seq, int do_index, 
 {
     void *args[] = {(void *)&a,       (void *)&n_frames,  (void *)&stats_seq,   (void *)&do_index,
                     (void *)&mailbox, (void *)&linger_ns, (void *)&next_request};
-    return status(cudaLaunchCooperativeKernel((const void *)k_frames, dim3(grid), dim3(CHUNK), args,
-                                              FRAMES_DYN_SMEM, st));
+    const void *kernel = wide(&a.pool) ? (const void *)k_frames<4> : (const void *)k_frames<2>;
+    return status(cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(CHUNK), args, FRAMES_DYN_SMEM, st));
 }
 
 inline bool staged(const cbtm_pool *pool) { return (pool->flags & CBTM_POOL_STAGED_LAUNCHES) != 0; }
@@ -391,7 +395,7 @@ int cbtm_update_finish(const cbtm_pool *pool, const cbtm_verdict *verdict, uintp
     FrameArgs a;
     rc = fill_args(pool, verdict, &a);
     if (rc) return rc;
-    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth);
+    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth, wide(pool));
     if (!grid) return finish_staged(a, nullptr, true, as_stream(stream));
     return frames_launch(a, 1, nullptr, 0, grid, as_stream(stream));
 }
@@ -404,7 +408,7 @@ int cbtm_update(const cbtm_pool *pool, const cbtm_verdict *verdict, uintptr_t st
     FrameArgs a;
     rc = fill_args(pool, verdict, &a);
     if (rc) return rc;
-    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth);
+    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth, wide(pool));
     if (!grid) {
         rc = index_launch(pool, true, as_stream(stream));
         return rc ? rc : finish_staged(a, nullptr, false, as_stream(stream));
@@ -486,7 +490,7 @@ int cbtm_run_epochs(const cbtm_pool *pool, const cbtm_verdict *verdict, int32_t 
     FrameArgs a;
     rc = fill_args(pool, verdict, &a);
     if (rc) return rc;
-    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth);
+    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth, wide(pool));
     for (int32_t done = 0; done < n_frames;) {
         const int32_t batch = n_frames - done < MAX_SEQ_FRAMES ? n_frames - done : MAX_SEQ_FRAMES;
         rc = status(cudaMemsetAsync(&a.ws.ctl->seq_frame, 0, sizeof(uint32_t), st));
@@ -519,7 +523,7 @@ int cbtm_update_linger(const cbtm_pool *pool, const cbtm_verdict *verdict, const
     FrameArgs a;
     rc = fill_args(pool, verdict, &a);
     if (rc) return rc;
-    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth);
+    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth, wide(pool));
     if (!grid) { // no cooperative launch: a plain update, nothing lingers
         rc = index_launch(pool, true, as_stream(stream));
         return rc ? rc : finish_staged(a, nullptr, false, as_stream(stream));
@@ -560,7 +564,7 @@ int cbtm_run_lod_sequence(const cbtm_pool *pool, const double *root_tris, const 
     rc = fill_args(pool, &v, &a);
     if (rc) return rc;
     a.use_prm_seq = 1;
-    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth);
+    const unsigned grid = staged(pool) ? 0 : persistent_grid(pool->depth, wide(pool));
     for (int32_t done = 0; done < n_frames;) {
         const int32_t batch = n_frames - done < MAX_SEQ_FRAMES ? n_frames - done : MAX_SEQ_FRAMES;
         rc = status(cudaMemcpyAsync(a.ws.prm_seq, prm_host + (size_t)CBTM_PRM_WORDS * done,

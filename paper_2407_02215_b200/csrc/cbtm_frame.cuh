@@ -78,7 +78,7 @@ struct Control {
     int64_t i0;         // first rank rejected by admission (n if none)
     int32_t tail_count;
     uint32_t seq_frame; // index into prm_seq for sequence runs
-    unsigned long long need_total; // fast path: warps done << 40 | sum of their needs (zero between frames)
+    unsigned long long need_total; // sum of the frame's reservation needs (zero between frames)
     int32_t mb_go;                 // linger mode: 1 = a request arrived in time, run another frame
     int32_t mb_pad_;
     double mb_prm[CBTM_PRM_WORDS]; // linger mode: the camera parameters of that request
@@ -92,7 +92,6 @@ struct Control {
 #endif
 };
 
-constexpr int NEED_TOTAL_SHIFT = 40; // sum of needs < 2^30 * 187 < 2^38; warps of the live ranks < 2^24 on the fast path
 
 struct Workspace {
     uint8_t *need8;   // [N] by live rank: slots to reserve (0 = no command)
@@ -414,6 +413,18 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
     const bool fast = fits_a_priori(p, n); // nothing can be rejected: scatter right away
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+    // frame totals (need, deepest bisector): accumulated per warp in registers over all its chunks, then
+    // per CTA in shared memory -- ONE global atomic per CTA and phase (one per warp and chunk put up to
+    // 60 000 atomics per frame on a single address: same-address atomics serialise in L2)
+    __shared__ unsigned long long s_need;
+    __shared__ int s_depth;
+    unsigned long long acc_need = 0;
+    int acc_depth = 0;
+    if (tid == 0) {
+        s_need = 0;
+        s_depth = 0;
+    }
+
     // the camera parameters of a sequence run sit behind two dependent loads (frame index, then
     // the row): issued now, parked in a register, put into shared memory only when the first
     // verdict needs them -- the record gathers below run meanwhile
@@ -435,23 +446,25 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
             s = p.cache_live[i];
             const uint64_t id = p.ids[s];
             const int32_t nx = p.nexts[s], pv = p.prevs[s];
-            // what a merge request will ask about its sibling and the opposite pair: gathered now,
-            // for everybody, so that the round trip hides behind the classifier
+            // what a merge request will ask about its sibling and the opposite pair: with the LOD
+            // classifier gathered now, for everybody, so that the round trip hides behind the fp64 work;
+            // the other verdict sources are known at once, so only merge requests gather (three scattered
+            // sectors per bisector saved: at 10^6 live bisectors this phase is bound by L2 transactions)
             const bool odd = id & 1;
             const int32_t sib = odd ? pv : nx, oth = odd ? nx : pv;
             uint64_t js = 0, jo = 0;
             int32_t j4 = -1;
-            if (sib >= 0) js = p.ids[sib];
-            if (oth >= 0) {
+            const bool gather = a.vmode == CBTM_VERDICT_LOD || verdict_of(a, prm, id, i) == 2;
+            if (gather && sib >= 0) js = p.ids[sib];
+            if (gather && oth >= 0) {
                 jo = p.ids[oth];
                 j4 = odd ? p.nexts[oth] : p.prevs[oth];
             }
             gathered = {id, js, jo, sib, oth, j4, nx, pv};
         }
-        { // deepest live bisector of the frame (one reduction + one fire-and-forget atomic per warp)
+        { // deepest live bisector of the frame
             const int d = i < n ? depth_of(gathered.id, p.rank) : 0;
-            const int dmax = __reduce_max_sync(FULL_MASK, d);
-            if (lane == 0 && dmax > 0) atomicMax((long long *)&ctl->stats[CBTM_STAT_PEAK_DEPTH], (long long)dmax);
+            acc_depth = max(acc_depth, __reduce_max_sync(FULL_MASK, d));
         }
         if (prm_pending) { // CTA-uniform
             if (tid < CBTM_PRM_WORDS) prm[tid] = prm_reg;
@@ -488,8 +501,7 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
         WORK_END(ctl, 0);
 #endif
         uint32_t sum = warp_sum(need);
-        // the frame's total need: one fire-and-forget atomic per warp (warps-done count above, needs below)
-        if (lane == 0) atomicAdd(&ctl->need_total, (unsigned long long)sum | (1ull << NEED_TOTAL_SHIFT));
+        acc_need += sum; // the frame's total need
         if (fast) {
             if (need == 2)
                 atomicOr(&p.commands[s], mbits);
@@ -518,13 +530,23 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
         __syncthreads();
     }
 
+    __syncthreads();
+    if (lane == 0) {
+        if (acc_need) atomicAdd(&s_need, acc_need);
+        if (acc_depth) atomicMax(&s_depth, acc_depth);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (s_need) atomicAdd(&ctl->need_total, s_need);
+        if (s_depth) atomicMax((long long *)&ctl->stats[CBTM_STAT_PEAK_DEPTH], (long long)s_depth);
+    }
 }
 
 // The frame's total need (complete behind the barrier that ends P2) and whether all of it fits.
 // Grid-uniform; need_total is zeroed by frame_totals, behind another barrier.
 __device__ __forceinline__ bool frame_fits(const FrameArgs &a, uint32_t n)
 {
-    const unsigned long long total = a.ws.ctl->need_total & ((1ull << NEED_TOTAL_SHIFT) - 1);
+    const unsigned long long total = a.ws.ctl->need_total;
     return total <= (((unsigned long long)1 << a.pool.depth) - n);
 }
 
@@ -535,7 +557,7 @@ __device__ __forceinline__ void frame_totals(const FrameArgs &a, uint32_t n, boo
     const cbtm_pool &p = a.pool;
     Control *ctl = a.ws.ctl;
     if (threadIdx.x == 0) {
-        const unsigned long long total = ctl->need_total & ((1ull << NEED_TOTAL_SHIFT) - 1);
+        const unsigned long long total = ctl->need_total;
         ctl->need_total = 0;
         if (fits) {
             ctl->n = n;
@@ -1413,7 +1435,12 @@ __global__ void __launch_bounds__(CHUNK) k_publish(const __grid_constant__ Frame
 // ---------------------------------------------------------------------------
 constexpr int FRAMES_DYN_SMEM = IDX_WARPS * IDX_STAGE_WORDS * 4; // 36 KB: index staging
 
-__global__ void __launch_bounds__(CHUNK, 2)
+// CTAS = co-resident CTAs per SM the register budget is cut for: 2 (latency-bound frames of a few hundred
+// chunks: fewer CTAs, cheaper barriers, no spills) or 4 (CBTM_POOL_WIDE_GRID, pools with 10^5 .. 10^7 live
+// bisectors: a CTA works through its chunks one after the other, each a chain of round trips, so twice the
+// CTAs in flight is close to twice the throughput)
+template <int CTAS>
+__global__ void __launch_bounds__(CHUNK, CTAS)
 k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, int do_index,
          const volatile int64_t *mailbox, long long linger_ns, long long next_request)
 {

@@ -29,6 +29,8 @@ MERGE_REQ = 8
 MERGE_QUAD = 16
 MERGE_OWNER = 32
 
+WIDE_GRID_LIVE = 150_000  # live bisectors from which the 4-CTAs-per-SM frame kernel is used
+
 _SNAPSHOT_DTYPES = {
     "ids": np.uint64, "nexts": np.int32, "prevs": np.int32, "twins": np.int32,
     "commands": np.uint32, "reserved": np.int32, "counter": np.int64,
@@ -124,15 +126,18 @@ class TriangulationState:
     def c_pool(self) -> _lib.CPool:
         """The cbtm_pool view of this state (cached; max_depth and the mode flags
         are plain attributes a caller may change between updates)."""
-        key = (int(self.max_depth), self.exact_free_cache, self.staged_launches, self.descend_free_ranks)
+        # wide grid (4 CTAs per SM) once the pool holds more live bisectors than the narrow grid has
+        # threads for two chunks each; decided from the last published live count (host-mapped stats)
+        wide = int(self._stats_np[7]) > WIDE_GRID_LIVE
+        key = (int(self.max_depth), self.exact_free_cache, self.staged_launches, self.descend_free_ranks, wide)
         cached = getattr(self, "_c_pool", None)
         if cached is not None and cached[0] == key:
             return cached[1]
-        pool = self._build_c_pool()
+        pool = self._build_c_pool(wide)
         self._c_pool = (key, pool)
         return pool
 
-    def _build_c_pool(self) -> _lib.CPool:
+    def _build_c_pool(self, wide: bool = False) -> _lib.CPool:
         p = _lib.ptr
         return _lib.CPool(
             p(self.d_ids), p(self.d_nexts), p(self.d_prevs), p(self.d_twins),
@@ -143,7 +148,8 @@ class TriangulationState:
             self.rank, int(self.max_depth),
             (_lib.POOL_FULL_FREE_CACHE if self.exact_free_cache else 0)
             | (_lib.POOL_STAGED_LAUNCHES if self.staged_launches else 0)
-            | (_lib.POOL_DESCEND_FREE_RANKS if self.descend_free_ranks else 0))
+            | (_lib.POOL_DESCEND_FREE_RANKS if self.descend_free_ranks else 0)
+            | (_lib.POOL_WIDE_GRID if wide else 0))
 
     def _touched(self) -> None:
         """The device arrays changed: drop host snapshots."""
