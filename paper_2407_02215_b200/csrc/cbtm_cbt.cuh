@@ -616,22 +616,36 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
             const uint32_t zline = (o1 + cnt + 31u) & ~31u;
             const uint32_t z0 = zline + (zeros_before & 31u);
             uint32_t p1 = o1, p0 = z0;
-            if (g.span == 1024u) { // every word fully valid (all pools with D >= 10)
+            if (g.span == 1024u && want_free) { // decode-all: every slot goes to exactly one of the two lists
+                // one select and ONE store per word: the staging index is p1 + r1 for a set bit and
+                // p0 + lane - r1 for a clear one (this loop is bound by instruction issue)
+                const uint32_t own = own_full;
+                uint32_t p0l = p0 + (uint32_t)lane;
+#pragma unroll 8
+                for (int w = 0; w < 32; ++w) {
+                    const uint32_t word = __shfl_sync(FULL_MASK, own, w);
+                    const uint32_t r1 = __popc(word & lane_lt);
+                    const bool bit = (word >> lane) & 1u;
+                    const int32_t slot = base + w * 32 + lane;
+                    st[bit ? p1 + r1 : p0l - r1] = slot;
+                    if (RESET && bit) reset_cmds[slot] = 0u;
+                    const uint32_t c = __popc(word);
+                    p1 += c;
+                    p0l += 32u - c;
+                }
+            } else if (g.span == 1024u) { // every word fully valid (all pools with D >= 10)
                 const uint32_t own = own_full;
 #pragma unroll 8
                 for (int w = 0; w < 32; ++w) {
                     const uint32_t word = __shfl_sync(FULL_MASK, own, w);
-                    if (word == 0u && !want_free) continue;
+                    if (word == 0u) continue;
                     const uint32_t r1 = __popc(word & lane_lt);
                     const int32_t slot = base + w * 32 + lane;
                     if ((word >> lane) & 1u) {
                         st[p1 + r1] = slot;
                         if (RESET) reset_cmds[slot] = 0u; // stage 3 (kernels.py:256-259)
-                    } else if (want_free)
-                        st[p0 + (uint32_t)lane - r1] = slot;
-                    const uint32_t c = __popc(word);
-                    p1 += c;
-                    p0 += 32u - c;
+                    }
+                    p1 += __popc(word);
                 }
             } else { // tiny pool: a single partial block
                 const uint32_t nwords = (g.span + 31u) / 32u;
