@@ -382,3 +382,47 @@ def conformity_violations(state: TriangulationState) -> list[str]:
             out.append(f"interior edge {key} owned by single triangle "
                        f"{who[0]} (T-junction)")
     return out
+
+
+# my vertex -> neighbour's vertex across a pointer, keyed by (my role, the role under which the
+# neighbour points back): which corners of the two decoded triangles must coincide.  Twins of equal
+# depth share the bisection edge reversed; the mixed pairs are a triangle meeting a neighbour one
+# level up or down (reference: _ADJ_CORRESPONDENCE, state.py:271-279; paper Table 1).
+_SHARED_CORNERS = {
+    ("twin", "twin"): {0: 1, 1: 0},
+    ("next", "prev"): {1: 0, 2: 2},
+    ("prev", "next"): {2: 2, 0: 1},
+    ("next", "twin"): {1: 0, 2: 1},
+    ("prev", "twin"): {2: 0, 0: 1},
+    ("twin", "next"): {0: 1, 1: 2},
+    ("twin", "prev"): {0: 2, 1: 0},
+}
+
+
+def adjacency_geometry_violations(state: TriangulationState) -> list[str]:
+    """Every pointer must join geometrically coincident edges with the corner
+    correspondence its role pair implies (state.py:282-313 of the reference).
+    Host-side checker on the GPU-decoded live triangles."""
+    ids, tris = state.decode_live()
+    live = state.live_slots()
+    where = {int(s): k for k, s in enumerate(live)}
+    arrays = {"next": state.nexts, "prev": state.prevs, "twin": state.twins}
+    out = []
+    for s, k in where.items():
+        for role, arr in arrays.items():
+            q = int(arr[s])
+            if q == -1:
+                continue
+            back = [r for r in _BACK_ROLES[role] if int(arrays[r][q]) == s]
+            if len(back) != 1 or q not in where:
+                out.append(f"slot {s} ({role}) -> {q}: back roles {back}")
+                continue
+            corners = _SHARED_CORNERS.get((role, back[0]))
+            if corners is None:
+                out.append(f"slot {s} ({role}) -> {q}: illegal role pair {(role, back[0])}")
+                continue
+            for mine, theirs in corners.items():
+                if _qpoint(tris[k][mine]) != _qpoint(tris[where[q]][theirs]):
+                    out.append(f"slot {s} ({role}) -> {q}: vertex {mine} != neighbor vertex "
+                               f"{theirs} under role pair {(role, back[0])}")
+    return out
