@@ -57,10 +57,12 @@ def from_reference_state(ref, st: TriangulationState) -> None:
 
 def _on_host_copy(name):
     def call(state, *args, **kw):
-        seq = _ref()[0]
+        seq, rstate, _ = _ref()
         ref = to_reference_state(state)
         try:
             return getattr(seq, name)(ref, *args, **kw)
+        except rstate.CapacityError as exc:      # the drop-in's exception type, as the tests import it
+            raise CapacityError(str(exc)) from None
         finally:
             from_reference_state(ref, state)
     call.__name__ = name
