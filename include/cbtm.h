@@ -50,7 +50,7 @@ extern "C" {
 #define CBTM_E_WORKSPACE 3 /* workspace smaller than cbtm_workspace_bytes */
 #define CBTM_E_MODE 4      /* unknown verdict mode / flag */
 #define CBTM_E_RANGE 5     /* count / size argument out of range */
-#define CBTM_E_ALIGN 6     /* bits, reserved, cache_live, cache_free must be 16-byte aligned */
+#define CBTM_E_ALIGN 6     /* bits, counters, reserved, cache_live, cache_free must be 16-byte aligned */
 #define CBTM_E_TIMEOUT 7   /* cbtm_wait_frame gave up */
 
 /* command-word bits (state.py:17-25) */
@@ -158,7 +158,10 @@ typedef struct cbtm_verdict {
 int cbtm_abi_version(void);
 /* number of u64 words of the bitfield (>= 16: one 128-byte line) */
 size_t cbtm_bitfield_words(int depth);
-/* number of u32 entries of the counter heap (index 0 unused) */
+/* number of u32 entries of the counter heap.  Index 0 is not a node: the library keeps a
+ * stamp there ("the levels above the tile roots are mutually consistent", which lets a full
+ * reduction update them by deltas instead of rebuilding them).  A caller that writes the
+ * counter array by other means than these entry points must zero counters[0]. */
 size_t cbtm_counter_words(int depth);
 /* scratch bytes needed by cbtm_update / cbtm_sum_reduce for one pool */
 size_t cbtm_workspace_bytes(int depth);

@@ -53,47 +53,75 @@ class Cbt:
                                dtype=t.uint8, device=self.device)
         self._bits, self._counters, self._scratch = _bits, _counters, _scratch
         self._mirror: np.ndarray | None = None  # host heap, reference layout
+        self._shadow: np.ndarray | None = None  # leaves as last synchronised with the device
         self._mirror_stale = True    # device holds newer data than the mirror
-        self._mirror_handed_out = False  # caller may have written the mirror
+        self._mirror_handed_out = False  # a caller holds a writable view of the mirror
         self._dirty = False
 
     # -- coherence between the host mirror and the device ------------------
+    # The reference's ``nodes`` / ``leaves`` are live views of the one heap array: a caller may
+    # keep the returned array and write it at any time (``lv = cbt.leaves; lv[a] = 1;
+    # cbt.sum_reduce(); lv[b] = 1; cbt.sum_reduce()``).  Once a view has been handed out the
+    # mirror therefore stays authoritative for the leaves the caller wrote: ``_shadow`` remembers
+    # the leaves as they were when mirror and device last agreed, every device operation first
+    # pushes whatever differs from it, and a refresh from the device keeps such writes.
     def _stream(self) -> int:
         return _lib.stream_handle(self.device)
+
+    def _export(self) -> np.ndarray:
+        t = _lib.torch()
+        dev = t.empty(2 * self.capacity, dtype=t.int32, device=self.device)
+        rc = _lib.load().cbtm_export_nodes(
+            _lib.ptr(self._bits), _lib.ptr(self._counters), self.depth,
+            _lib.ptr(dev), self._stream())
+        _lib.check(rc, "cbtm_export_nodes")
+        return _lib.to_host(dev, np.uint32)
+
+    def _caller_writes(self) -> np.ndarray | None:
+        """Leaf positions the holder of a view changed since the last synchronisation."""
+        if self._mirror is None or not self._mirror_handed_out:
+            return None
+        diff = np.flatnonzero(self._mirror[self.capacity:] != self._shadow)
+        return diff if diff.size else None
 
     def _pull(self) -> np.ndarray:
         """Host mirror of the heap, refreshed from the device if needed."""
         if self._mirror is None or self._mirror_stale:
-            t = _lib.torch()
-            dev = t.empty(2 * self.capacity, dtype=t.int32, device=self.device)
-            rc = _lib.load().cbtm_export_nodes(
-                _lib.ptr(self._bits), _lib.ptr(self._counters), self.depth,
-                _lib.ptr(dev), self._stream())
-            _lib.check(rc, "cbtm_export_nodes")
-            fresh = _lib.to_host(dev, np.uint32)
+            fresh = self._export()
             if self._mirror is None:
                 self._mirror = fresh.copy()
             else:
+                written = self._caller_writes()
+                kept = None if written is None else self._mirror[self.capacity + written].copy()
                 self._mirror[...] = fresh
+                if written is not None:      # writes made through a held view survive the refresh
+                    self._shadow = fresh[self.capacity:].copy()
+                    self._mirror[self.capacity + written] = kept
+                    self._mirror_stale = False
+                    self._dirty = True
+                    return self._mirror
+            self._shadow = self._mirror[self.capacity:].copy()
             self._mirror_stale = False
         return self._mirror
 
     def _push(self) -> None:
         """Push leaves the caller may have written into the mirror."""
-        if self._mirror is None or not self._mirror_handed_out:
+        if self._caller_writes() is None:    # host-only comparison: no device traffic when nothing was written
             return
+        if self._mirror_stale:
+            self._pull()                     # merges held-view writes into the device's newer leaves
         leaves = np.ascontiguousarray(self._mirror[self.capacity:])
         dev = _lib.to_device(leaves, self.device)
         rc = _lib.load().cbtm_import_leaves(_lib.ptr(self._bits), self.depth,
                                             _lib.ptr(dev), self._stream())
         _lib.check(rc, "cbtm_import_leaves")
         _lib.torch().cuda.current_stream(self.device).synchronize()
-        self._mirror_handed_out = False
+        self._shadow = leaves.copy()
+        self._mirror_stale = True            # internal nodes of the mirror are out of date until the next pull
 
     def _device_changed(self, dirty: bool) -> None:
         """Called by the update engine after it rewrote bits/counters."""
         self._mirror_stale = True
-        self._mirror_handed_out = False
         self._dirty = dirty
 
     # -- leaf access -------------------------------------------------------
@@ -133,6 +161,8 @@ class Cbt:
         _lib.check(rc, "cbtm_sum_reduce")
         self._mirror_stale = True
         self._dirty = False
+        if self._mirror_handed_out:
+            self._pull()    # a held ``nodes`` view shows the new sums in place, as the reference's array does
 
     def count(self) -> int:
         assert not self._dirty, "sum_reduce required before count()"
@@ -214,6 +244,7 @@ def _cbt_from_heap(nodes: np.ndarray, depth: int) -> Cbt:
     c = Cbt(depth, max_depth=HARD_MAX_DEPTH)
     c._mirror = np.zeros(2 * cap, np.uint32)
     c._mirror[cap:] = nodes[cap:2 * cap]
+    c._shadow = np.zeros(cap, np.uint32)   # the fresh device field is empty
     c._mirror_stale = False
     c._mirror_handed_out = True
     c.sum_reduce()

@@ -6,6 +6,8 @@
 //        --shared -Xcompiler -fPIC -o libcbtm.so cbtm.cu
 #include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "cbtm_frame.cuh"
@@ -15,18 +17,35 @@ using namespace cbtm;
 
 namespace {
 
-int g_sm_count = 0;
+// Per-device properties, cached per device ordinal (a process may drive several GPUs).
+constexpr int MAX_DEVICES = 64;
+struct DeviceInfo {
+    std::atomic<int> sm_count{0};
+    std::atomic<int> reduce_smem_opt_in{0};
+    std::atomic<int> frame_ctas_per_sm[2] = {{0}, {0}};
+    std::atomic<int> batch_ctas_per_sm{0};
+};
+DeviceInfo g_devices[MAX_DEVICES];
+
+inline DeviceInfo &device_info()
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAX_DEVICES) dev = 0;
+    return g_devices[dev];
+}
 
 inline int sm_count()
 {
-    if (g_sm_count == 0) {
-        int dev = 0, n = 0;
+    DeviceInfo &d = device_info();
+    int n = d.sm_count.load(std::memory_order_relaxed);
+    if (n == 0) {
+        int dev = 0;
         if (cudaGetDevice(&dev) != cudaSuccess ||
             cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
             n = 148; // B200
-        g_sm_count = n;
+        d.sm_count.store(n, std::memory_order_relaxed); // (racing threads store the same value)
     }
-    return g_sm_count;
+    return n;
 }
 
 inline int status(cudaError_t e) { return e == cudaSuccess ? 0 : -(int)e; }
@@ -43,37 +62,63 @@ inline unsigned strided_grid(uint64_t units, uint64_t per_cta, int ctas_per_sm)
     return want ? (unsigned)want : 1u;
 }
 
-int reduce_launch(const uint64_t *bits, uint32_t *counters, int depth, unsigned *ticket,
-                  const ReducePublish &pub, cudaStream_t st)
+// tuning hook for benchmarks/reduce_sweep.py: "ctas_per_sm,max_stages" (unset: the policy below)
+inline bool reduce_tuning(unsigned *ctas_per_sm, unsigned *max_stages)
 {
-    static bool smem_opt_in = false;
-    if (!smem_opt_in) {
+    static const char *env = getenv("CBTM_REDUCE_TUNE");
+    if (!env) return false;
+    unsigned a = 0, b = 0;
+    if (sscanf(env, "%u,%u", &a, &b) != 2 || a < 1 || a > 8 || b < 1 || b > (unsigned)RED_MAX_STAGES) return false;
+    *ctas_per_sm = a, *max_stages = b;
+    return true;
+}
+
+int reduce_launch(const uint64_t *bits, uint32_t *counters, int depth, unsigned *ticket, cudaStream_t st)
+{
+    DeviceInfo &d = device_info();
+    if (!d.reduce_smem_opt_in.load(std::memory_order_acquire)) {
         const cudaError_t e = cudaFuncSetAttribute(k_sum_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    RED_MAX_STAGES * RED_TILE_BYTES);
         if (e != cudaSuccess) return status(e);
-        smem_opt_in = true;
+        d.reduce_smem_opt_in.store(1, std::memory_order_release);
     }
     const Geo g = make_geo(depth);
     const unsigned tiles = g.nblocks > (unsigned)RED_TILE_BLOCKS ? g.nblocks / RED_TILE_BLOCKS : 1u;
     const uint64_t total_bytes = (uint64_t)bitfield_words(depth) * 8;
-    // few tiles: one CTA per tile, all resident; many: 3 CTAs per SM, each streaming
-    // its range through a 4-stage (64 KB) ring
+    // Each CTA streams its tiles through a ring of 16 KB stages; every stage is a TMA bulk copy in
+    // flight.  Up to four tiles per SM (2^26): one CTA per tile, everything resident and in flight
+    // at once.  Beyond that: 3 CTAs per SM with two stages each -- 14 MB in flight, twice what
+    // the HBM pipe needs -- of which only the first two tiles are dealt statically; the rest are
+    // claimed as stages free up, so that SMs which stream faster take more tiles (measured:
+    // 4 stages -> 2^28 13.3 us, 2 stages -> 9.7 us; 2^30 the same 29 us).
+    unsigned ctas_per_sm = 3, max_stages = 2;
+    const bool tuned = reduce_tuning(&ctas_per_sm, &max_stages);
+    const unsigned sms = (unsigned)sm_count();
     unsigned grid = tiles;
-    int stages = 1;
-    const unsigned resident = (unsigned)sm_count() * 4;
-    if (tiles > resident) {
-        grid = (unsigned)sm_count() * 3;
-        const unsigned per_cta = (tiles + grid - 1) / grid;
-        stages = per_cta < (unsigned)RED_MAX_STAGES ? (int)per_cta : RED_MAX_STAGES;
-    }
-    // the last CTA reuses the ring as a heap of 2 * tiles words
+    if (tuned) grid = tiles < sms * ctas_per_sm ? tiles : sms * ctas_per_sm;
+    else if (tiles > 4 * sms) grid = sms * ctas_per_sm;
+    const unsigned per_cta = (tiles + grid - 1) / grid;
+    unsigned stages = per_cta < max_stages ? per_cta : max_stages;
+    // a tree that was never built is finished by the last CTA, which reuses the ring as a heap
+    // of 2 * tiles words
     while ((size_t)stages * RED_TILE_BYTES < (size_t)tiles * 8) ++stages;
-    k_sum_reduce<<<grid, RED_THREADS, (size_t)stages * RED_TILE_BYTES, st>>>(
-        reinterpret_cast<const uint8_t *>(bits), counters, g.lc, total_bytes, tiles, stages, ticket, pub);
-    return launch_status();
-}
 
-const ReducePublish kNoPublish = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(RED_THREADS);
+    cfg.dynamicSmemBytes = (size_t)stages * RED_TILE_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    // programmatic dependent launch: this grid's CTAs may be scheduled while the previous kernel
+    // of the stream drains; the kernel waits (griddepcontrol.wait) before it touches memory
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    static const bool no_pdl = getenv("CBTM_REDUCE_NO_PDL") != nullptr; // measurement hook
+    cfg.attrs = attr;
+    cfg.numAttrs = no_pdl ? 0 : 1;
+    return status(cudaLaunchKernelEx(&cfg, k_sum_reduce, reinterpret_cast<const uint8_t *>(bits), counters, g.lc,
+                                     total_bytes, tiles, (int)stages, ticket));
+}
 
 int check_pool(const cbtm_pool *p, bool need_ws)
 {
@@ -88,7 +133,9 @@ int check_pool(const cbtm_pool *p, bool need_ws)
     }
     if (p->rank < 1 || p->rank > 62 || p->max_depth < 0) return CBTM_E_RANGE;
     // 128-bit accesses: reserved rows, index lists, bitfield lines
-    if (((uintptr_t)p->reserved | (uintptr_t)p->cache_live | (uintptr_t)p->cache_free | (uintptr_t)p->bits) & 15)
+    // (counters: the ranked descent reads eight sibling counters as two 128-bit loads)
+    if (((uintptr_t)p->reserved | (uintptr_t)p->cache_live | (uintptr_t)p->cache_free | (uintptr_t)p->bits |
+         (uintptr_t)p->counters) & 15)
         return CBTM_E_ALIGN;
     return 0;
 }
@@ -171,8 +218,10 @@ int finish_staged(const FrameArgs &a, int64_t *stats_seq, bool with_reset, cudaS
 // Co-resident grid of the persistent frame kernel (0: cooperative launch unavailable); wide = 4 CTAs per SM
 unsigned persistent_grid(int depth, bool wide = false)
 {
-    static int ctas_per_sm[2] = {-1, -1};
-    int &cached = ctas_per_sm[wide ? 1 : 0];
+    // cached per device as value + 1 (0 = not probed yet); the probe is idempotent, so racing
+    // threads store the same number
+    std::atomic<int> &slot = device_info().frame_ctas_per_sm[wide ? 1 : 0];
+    int cached = slot.load(std::memory_order_acquire) - 1;
     if (cached < 0) {
         const void *kernel = wide ? (const void *)k_frames<4> : (const void *)k_frames<2>;
         const int want_per_sm = wide ? 4 : 2;
@@ -185,6 +234,7 @@ unsigned persistent_grid(int depth, bool wide = false)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, CHUNK, FRAMES_DYN_SMEM) == cudaSuccess)
             cached = per_sm > want_per_sm ? want_per_sm : per_sm;
         (void)cudaGetLastError();
+        slot.store(cached + 1, std::memory_order_release);
     }
     if (cached <= 0) return 0;
     const uint64_t want = (((uint64_t)1 << depth) + CHUNK - 1) / CHUNK; // tiny pools: fewer CTAs, cheaper barriers
@@ -229,13 +279,20 @@ int cbtm_sum_reduce(const uint64_t *bits, uint32_t *counters, int depth, void *w
 {
     if (bad_depth(depth)) return CBTM_E_DEPTH;
     if (!bits || !counters || !workspace) return CBTM_E_NULL;
-    if ((uintptr_t)bits & 15) return CBTM_E_ALIGN; // TMA bulk copies
+    if (((uintptr_t)bits | (uintptr_t)counters) & 15) return CBTM_E_ALIGN; // TMA bulk copies; 128-bit counter loads
     if (workspace_bytes < 256) return CBTM_E_WORKSPACE;
-    // the ticket is word 0 of the workspace (also of a pool's frame workspace); it
-    // must be zero on entry and the last CTA leaves it zero again
-    return reduce_launch(bits, counters, depth, reinterpret_cast<unsigned *>(workspace), kNoPublish,
-                         as_stream(stream));
+    // words 0 and 1 of the workspace (also of a pool's frame workspace) are the rebuild ticket and
+    // the tile claim counter; both must be zero on entry and the kernel leaves them zero again
+    return reduce_launch(bits, counters, depth, reinterpret_cast<unsigned *>(workspace), as_stream(stream));
 }
+
+#ifdef CBTM_DEBUG_TIMING
+// debug builds only (benchmarks/reduce_probe.py): per-CTA stamps of the last k_sum_reduce launch
+extern "C" int cbtm_debug_reduce_stamps(unsigned long long *host_out, int n_ctas)
+{
+    return status(cudaMemcpyFromSymbol(host_out, g_reduce_stamps, sizeof(unsigned long long) * 5 * n_ctas));
+}
+#endif
 
 int cbtm_decode_ones(const uint64_t *bits, const uint32_t *counters, int depth, const int64_t *ranks,
                      int64_t K, int32_t *out, uintptr_t stream)
@@ -243,6 +300,7 @@ int cbtm_decode_ones(const uint64_t *bits, const uint32_t *counters, int depth, 
     if (bad_depth(depth)) return CBTM_E_DEPTH;
     if (!bits || !counters || (K > 0 && !out)) return CBTM_E_NULL;
     if (K < 0) return CBTM_E_RANGE;
+    if (((uintptr_t)bits | (uintptr_t)counters) & 15) return CBTM_E_ALIGN; // 128-bit loads of lines / sibling counters
     if (K == 0) return 0;
     k_decode<true><<<strided_grid((uint64_t)K, 256, 8), 256, 0, as_stream(stream)>>>(bits, counters, depth,
                                                                                    ranks, K, out);
@@ -255,6 +313,7 @@ int cbtm_decode_zeros(const uint64_t *bits, const uint32_t *counters, int depth,
     if (bad_depth(depth)) return CBTM_E_DEPTH;
     if (!bits || !counters || (K > 0 && !out)) return CBTM_E_NULL;
     if (K < 0) return CBTM_E_RANGE;
+    if (((uintptr_t)bits | (uintptr_t)counters) & 15) return CBTM_E_ALIGN; // 128-bit loads of lines / sibling counters
     if (K == 0) return 0;
     k_decode<false><<<strided_grid((uint64_t)K, 256, 8), 256, 0, as_stream(stream)>>>(bits, counters, depth,
                                                                                     ranks, K, out);
@@ -266,7 +325,7 @@ int cbtm_index(const uint64_t *bits, const uint32_t *counters, int depth, int32_
 {
     if (bad_depth(depth)) return CBTM_E_DEPTH;
     if (!bits || !counters || !cache_live) return CBTM_E_NULL;
-    if (((uintptr_t)bits | (uintptr_t)cache_live | (uintptr_t)cache_free) & 15) return CBTM_E_ALIGN;
+    if (((uintptr_t)bits | (uintptr_t)counters | (uintptr_t)cache_live | (uintptr_t)cache_free) & 15) return CBTM_E_ALIGN;
     const Geo g = make_geo(depth);
     k_index<false><<<strided_grid(g.nblocks, IDX_WARPS, 6), IDX_WARPS * 32, 0, as_stream(stream)>>>(
         reinterpret_cast<const uint32_t *>(bits), counters, depth, cache_live, cache_free, dispatch, nullptr);
@@ -306,7 +365,7 @@ int cbtm_initialize(const cbtm_pool *pool, const int32_t *he_next, const int32_t
         *pool, he_next, he_prev, he_twin, n_halfedges, ws);
     rc = launch_status();
     if (rc) return rc;
-    return reduce_launch(pool->bits, pool->counters, pool->depth, ws.ticket, kNoPublish, st);
+    return reduce_launch(pool->bits, pool->counters, pool->depth, ws.ticket, st);
 }
 
 int cbtm_root_triangles(const int32_t *he_next, const int32_t *he_vert, const double *positions,
@@ -619,7 +678,9 @@ int cbtm_run_lod_sequence_batch(const cbtm_pool *pools, int32_t n_pools, const d
         any_staged |= staged(&pools[q]);
     }
     if (n_frames == 0) return 0;
-    static int batch_per_sm = -1; // co-resident CTAs per SM of the batch kernel (0: no cooperative launch)
+    // co-resident CTAs per SM of the batch kernel (0: no cooperative launch); per device, value + 1
+    std::atomic<int> &batch_slot = device_info().batch_ctas_per_sm;
+    int batch_per_sm = batch_slot.load(std::memory_order_acquire) - 1;
     if (batch_per_sm < 0) {
         int per_sm = 0;
         batch_per_sm = 0;
@@ -630,6 +691,7 @@ int cbtm_run_lod_sequence_batch(const cbtm_pool *pools, int32_t n_pools, const d
                 cudaSuccess)
             batch_per_sm = per_sm > BATCH_CTAS_PER_SM ? BATCH_CTAS_PER_SM : per_sm;
         (void)cudaGetLastError();
+        batch_slot.store(batch_per_sm + 1, std::memory_order_release);
     }
     const int batch_ok = batch_per_sm > 0;
     if (!batch_ok || any_staged || n_pools == 1) { // one pool after the other (same results)

@@ -21,14 +21,16 @@ namespace cbtm {
 // shuffle butterflies; disjoint lanes hold one node each and write all 31 with
 // a single store instruction.  The three levels that join the eight warps cost
 // the one CTA barrier per tile that also recycles the stage.  Levels above the
-// tile roots are built by the last CTA to finish (ticket; only thread 0
-// fences -- the fence is cumulative over the preceding barrier).
+// tile roots: every tile adds the change of its root to its ancestors with
+// atomics (see TREE_STAMP); only a tree that was never built goes through a
+// last-CTA rebuild (ticket).
 // HBM traffic: N/8 bytes read + 4 * (2 << Lc) = N/128 bytes written.
 // ---------------------------------------------------------------------------
 constexpr int RED_THREADS = 256;
 constexpr int RED_TILE_BYTES = 16384;
 constexpr int RED_TILE_BLOCKS = 128; // leaf blocks per tile
 constexpr int RED_MAX_STAGES = 4;
+constexpr uint32_t RED_NO_TILE = 0xffffffffu;
 
 // end-of-frame bookkeeping (publish_frame)
 struct ReducePublish {
@@ -98,6 +100,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
                  : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
     asm volatile(
@@ -122,6 +129,22 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
                  : "memory");
 }
 
+// counters[0] is padding in the heap layout; the library keeps a stamp there that says "every
+// counter above the tile roots equals the sum of its children" (true after any full build and
+// kept true by the in-frame reducer).  With the stamp present a full reduction does not rebuild
+// those levels: each tile adds the CHANGE of its root to its ancestors with fire-and-forget
+// atomics, so the kernel has no last-CTA pass, no ticket and no fence.  Without it (fresh or
+// foreign counters) the last CTA to finish rebuilds them and sets the stamp.
+constexpr uint32_t TREE_STAMP = 0x31544243u; // "CBT1"
+
+// Programmatic dependent launch: the CTAs of the next PDL-launched kernel on the stream may be
+// scheduled (and run their prologue up to griddep_wait) while this grid is still running.
+__device__ __forceinline__ void griddep_launch_dependents()
+{
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Levels above `cnt` subtree roots (counters[cnt .. 2 cnt), cnt a power of two >= 2),
 // built by the last CTA to arrive (ticket; only thread 0 fences -- the fence is
 // cumulative over the preceding barrier).  Binary heap in shared memory (`heap`,
@@ -130,8 +153,7 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 // copy-out of all internal nodes (walking the levels through L2 instead costs a
 // round trip per level).  All nb CTAs must call it.
 __device__ __forceinline__ void finish_upper_tree(uint32_t *counters, uint32_t cnt, unsigned *ticket,
-                                                  const ReducePublish &pub, uint32_t *heap, bool *is_last,
-                                                  uint32_t nb)
+                                                  uint32_t *heap, bool *is_last, uint32_t nb)
 {
     const int t = threadIdx.x;
     __syncthreads();
@@ -161,73 +183,123 @@ __device__ __forceinline__ void finish_upper_tree(uint32_t *counters, uint32_t c
         __syncthreads();
     }
     for (uint32_t i = 1 + t; i < cnt; i += RED_THREADS) counters[i] = heap[i];
-    if (t == 0) *ticket = 0;
-    publish_frame(pub, heap[1], t);
+    if (t == 0) {
+        *ticket = 0;
+        counters[0] = TREE_STAMP;
+    }
     __syncthreads();
 }
 
-// Per-CTA state of the TMA ring that survives across frames of a persistent
-// kernel: barriers are initialised once, `iter` counts the tiles this CTA has
-// pushed through the ring so far (stage = iter % stages, parity = iter / stages).
-struct ReduceRing {
-    uint8_t *ring;   // stages x 16 KB of shared memory (also the upper-tree heap)
-    uint64_t *full;  // RED_MAX_STAGES mbarriers
-    uint32_t (*wroot)[RED_THREADS / 32]; // [2][8]
-    bool *is_last;
-    int stages;
-    uint32_t iter;
-};
+#ifdef CBTM_DEBUG_TIMING
+// per CTA: kernel entry, released by griddepcontrol.wait, first tile landed, last tile counted, SM id
+__device__ unsigned long long g_reduce_stamps[8192 * 5];
+#define RED_STAMP(slot)                                                                                           \
+    do {                                                                                                          \
+        if (threadIdx.x == 0 && blockIdx.x < 8192) g_reduce_stamps[blockIdx.x * 5 + (slot)] = global_ns();        \
+    } while (0)
+#else
+#define RED_STAMP(slot)
+#endif
 
-__device__ __forceinline__ void reduce_ring_init(ReduceRing &rr)
+// One full sum reduction by the grid (Cbt.sum_reduce, initialize, BASELINE config 4).
+__global__ void __launch_bounds__(RED_THREADS)
+k_sum_reduce(const uint8_t *bits, uint32_t *counters, int lc, uint64_t total_bytes, uint32_t n_tiles,
+             int n_stages, unsigned *ticket)
 {
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < rr.stages; ++s) mbar_init(&rr.full[s], 1);
+    extern __shared__ __align__(128) uint8_t ring[]; // n_stages x 16 KB (also the upper-tree heap)
+    __shared__ __align__(8) uint64_t full[RED_MAX_STAGES];
+    __shared__ uint32_t wroot[2][RED_THREADS / 32];
+    __shared__ uint32_t stage_tile[RED_MAX_STAGES]; // tile in flight per stage (RED_NO_TILE: none)
+    __shared__ bool is_last;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t bid = blockIdx.x, nb = gridDim.x;
+    const uint32_t stages = (uint32_t)n_stages;
+
+    RED_STAMP(0);
+    if (t == 0) {
+        for (uint32_t s = 0; s < stages; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    rr.iter = 0;
+    griddep_launch_dependents();
     __syncthreads();
-}
+    griddep_wait(); // nothing above touches global memory: the previous kernel's writes are visible from here on
+    RED_STAMP(1);
+#ifdef CBTM_DEBUG_TIMING
+    if (t == 0 && bid < 8192) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_reduce_stamps[bid * 5 + 4] = smid;
+    }
+#endif
 
-// One full sum reduction by the CTAs (bid of nb).  All nb CTAs must call it.
-__device__ __forceinline__ void reduce_phase(const uint8_t *bits, uint32_t *counters, int lc,
-                                             uint64_t total_bytes, uint32_t n_tiles, unsigned *ticket,
-                                             const ReducePublish &pub, ReduceRing &rr, uint32_t bid,
-                                             uint32_t nb)
-{
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const uint32_t stages = (uint32_t)rr.stages;
-    // tiles are dealt round-robin (tile = bid + k * nb): at any moment the CTAs read
-    // one contiguous window of the bitfield, which keeps DRAM rows open
-    const uint32_t my_tiles = bid < n_tiles ? (n_tiles - bid + nb - 1) / nb : 0u;
-    const uint32_t it0 = rr.iter;
-
+    // Tiles: the first `stages` of a CTA are dealt round-robin (tile = bid + s * nb); all further
+    // ones are CLAIMED from a global counter when a stage is refilled.  SMs do not stream at the
+    // same rate (near / far memory die), and with a static deal the slow ones set the kernel's
+    // duration (measured at 2^30: SMs finished between 22.6 and 31.0 us).  Either way the grid
+    // reads one moving contiguous window of the bitfield, which keeps DRAM rows open.  Every CTA
+    // makes exactly one claim that fails, so the counter sees n_tiles - nb * stages + nb
+    // increments per launch: atomicInc wraps it back to zero on the last one (no reset pass).
+    const uint32_t n_static = nb * stages;
+    const bool dynamic = n_tiles > n_static;
+    const uint32_t claim_wrap = n_tiles - n_static + nb - 1;
+    unsigned *claim_counter = ticket + 1;
     auto tile_bytes = [&](uint32_t tile) -> uint32_t {
         const uint64_t left = total_bytes - (uint64_t)tile * RED_TILE_BYTES;
         return left < RED_TILE_BYTES ? (uint32_t)left : (uint32_t)RED_TILE_BYTES;
     };
-    auto issue = [&](uint32_t tile, uint32_t it) {
-        const uint32_t stage = it % stages;
+    auto issue = [&](uint32_t tile, uint32_t stage) { // thread 0
+        stage_tile[stage] = tile; // (published to the CTA by the mbarrier's release / acquire)
+        if (tile == RED_NO_TILE) {
+            mbar_arrive(&full[stage]);
+            return;
+        }
         const uint32_t bytes = tile_bytes(tile);
-        mbar_expect_tx(&rr.full[stage], bytes);
-        bulk_load(rr.ring + (size_t)stage * RED_TILE_BYTES, bits + (size_t)tile * RED_TILE_BYTES, bytes,
-                  &rr.full[stage]);
+        mbar_expect_tx(&full[stage], bytes);
+        bulk_load(ring + (size_t)stage * RED_TILE_BYTES, bits + (size_t)tile * RED_TILE_BYTES, bytes, &full[stage]);
     };
-
+    uint32_t claimed = RED_NO_TILE; // thread 0: the claim in flight (posted one refill ahead, so its latency hides)
+    bool claiming = false;
     if (t == 0) {
-        // the ring may have been written through the generic proxy (index staging,
-        // upper-tree heap) since the last bulk copy
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        for (uint32_t k = 0; k < stages && k < my_tiles; ++k) issue(bid + k * nb, it0 + k);
+        for (uint32_t s = 0; s < stages; ++s) {
+            const uint32_t tile = bid + s * nb;
+            issue(tile < n_tiles ? tile : RED_NO_TILE, s);
+        }
+        if (dynamic) {
+            claimed = n_static + atomicInc(claim_counter, claim_wrap);
+            claiming = true;
+        }
     }
 
-    for (uint32_t k = 0; k < my_tiles; ++k) {
-        const uint32_t tile = bid + k * nb;
-        const uint32_t it = it0 + k;
-        const uint32_t stage = it % stages;
-        mbar_wait(&rr.full[stage], (it / stages) & 1u);
+    // The roots of the statically dealt tiles as the levels above still see them (delta mode; lane 6
+    // of warp 0 rewrites them).  Fetched now, unconditionally, next to the tiles themselves: after a
+    // cold start these words come from DRAM, and a load issued only once the tile has landed would
+    // sit on the CTA's critical path.
+    const int top = lc - 7; // level of the tile roots (n_tiles > 1)
+    uint32_t old0 = 0, old1 = 0, old2 = 0, old3 = 0;
+    if (t == 6 && n_tiles > 1) {
+        const uint32_t *roots = counters + (1u << top);
+        if (bid < n_tiles) old0 = __ldcg(roots + bid);
+        if (stages > 1 && bid + nb < n_tiles) old1 = __ldcg(roots + bid + nb);
+        if (stages > 2 && bid + 2 * nb < n_tiles) old2 = __ldcg(roots + bid + 2 * nb);
+        if (stages > 3 && bid + 3 * nb < n_tiles) old3 = __ldcg(roots + bid + 3 * nb);
+    }
+    // the same word for every CTA of the grid: only the rebuild path writes it, after the last ticket
+    const bool delta_mode = n_tiles > 1 && __ldcg(&counters[0]) == TREE_STAMP;
+
+    for (uint32_t k = 0;; ++k) {
+        const uint32_t stage = k % stages;
+        mbar_wait(&full[stage], (k / stages) & 1u);
+        const uint32_t tile = stage_tile[stage];
+        if (tile == RED_NO_TILE) break; // (uniform: every thread reads the same word)
+#ifdef CBTM_DEBUG_TIMING
+        if (k == 0) RED_STAMP(2);
+#endif
+        // claimed tiles: the refill prefetched the old root into L2
+        uint32_t old_root = k == 0 ? old0 : k == 1 ? old1 : k == 2 ? old2 : old3;
+        if (delta_mode && t == 6 && k >= stages) old_root = __ldcg(&counters[(1u << top) + tile]);
 
         // my 64 bytes of the tile; the rotation keeps the four LDS.128 conflict free
-        const uint4 *mine = reinterpret_cast<const uint4 *>(rr.ring + (size_t)stage * RED_TILE_BYTES) + t * 4;
+        const uint4 *mine = reinterpret_cast<const uint4 *>(ring + (size_t)stage * RED_TILE_BYTES) + t * 4;
         uint32_t c = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) c += popc128(mine[(j + (lane >> 1)) & 3]);
@@ -254,49 +326,48 @@ __device__ __forceinline__ void reduce_phase(const uint8_t *bits, uint32_t *coun
             val = l4, lvl = lc - 4, pos = tile * 8 + warp;
         }
         if (lvl >= 0 && pos < (1u << lvl)) counters[(1u << lvl) + pos] = val;
-        if (lane == 0) rr.wroot[k & 1][warp] = l4;
+        if (lane == 0) wroot[k & 1][warp] = l4;
         __syncthreads(); // stage consumed by everyone; warp roots visible
-        if (t == 0 && k + stages < my_tiles) issue(tile + stages * nb, it + stages);
-        if (warp == 0 && lane < 7) { // levels lc-5 (4 nodes), lc-6 (2), lc-7 (tile root)
-            const uint32_t *w = rr.wroot[k & 1];
-            uint32_t v2, p2;
-            int l5;
+        if (t == 0) { // refill the stage: the tile claimed one refill ago; post the next claim
+            uint32_t next = RED_NO_TILE;
+            if (claiming) {
+                if (claimed < n_tiles) {
+                    next = claimed;
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(counters + (1u << top) + next));
+                    claimed = n_static + atomicInc(claim_counter, claim_wrap);
+                } else {
+                    claiming = false;
+                }
+            }
+            issue(next, stage);
+        }
+        if (warp == 0) { // levels lc-5 (4 nodes), lc-6 (2), lc-7 (tile root); then the levels above
+            const uint32_t *w = wroot[k & 1];
+            uint32_t v2 = 0, p2 = 0;
+            int l5 = -1;
             if (lane < 4) {
                 v2 = w[2 * lane] + w[2 * lane + 1], l5 = lc - 5, p2 = tile * 4 + lane;
             } else if (lane < 6) {
                 const int q = (lane - 4) * 4;
                 v2 = w[q] + w[q + 1] + w[q + 2] + w[q + 3], l5 = lc - 6, p2 = tile * 2 + (lane - 4);
-            } else {
+            } else if (lane == 6) {
                 v2 = w[0] + w[1] + w[2] + w[3] + w[4] + w[5] + w[6] + w[7], l5 = lc - 7, p2 = tile;
             }
             if (l5 >= 0 && p2 < (1u << l5)) counters[(1u << l5) + p2] = v2;
+            if (delta_mode) { // lane l adds the change of the tile root to the ancestor on level l
+                const uint32_t delta = __shfl_sync(FULL_MASK, v2 - old_root, 6);
+                if (delta != 0 && lane < top) atomicAdd(&counters[(1u << lane) + (tile >> (top - lane))], delta);
+            }
         }
     }
-    rr.iter = it0 + my_tiles;
 
-    if (n_tiles == 1) { // the single tile's subtree is the whole tree (CTA 0 owns it)
-        if (bid == 0) {
-            const uint32_t *w = rr.wroot[0];
-            publish_frame(pub, w[0] + w[1] + w[2] + w[3] + w[4] + w[5] + w[6] + w[7], t);
-        }
-        __syncthreads();
+    RED_STAMP(3);
+    if (n_tiles == 1) { // the single tile's subtree is the whole tree
+        if (bid == 0 && t == 0) counters[0] = TREE_STAMP;
         return;
     }
-
-    finish_upper_tree(counters, n_tiles, ticket, pub, reinterpret_cast<uint32_t *>(rr.ring), rr.is_last, nb);
-}
-
-__global__ void __launch_bounds__(RED_THREADS)
-k_sum_reduce(const uint8_t *bits, uint32_t *counters, int lc, uint64_t total_bytes, uint32_t n_tiles,
-             int stages, unsigned *ticket, const ReducePublish pub)
-{
-    extern __shared__ __align__(128) uint8_t dyn_smem[]; // stages x 16 KB
-    __shared__ __align__(8) uint64_t full[RED_MAX_STAGES];
-    __shared__ uint32_t wroot[2][RED_THREADS / 32];
-    __shared__ bool is_last;
-    ReduceRing rr{dyn_smem, full, wroot, &is_last, stages, 0};
-    reduce_ring_init(rr);
-    reduce_phase(bits, counters, lc, total_bytes, n_tiles, ticket, pub, rr, blockIdx.x, gridDim.x);
+    if (delta_mode) return;
+    finish_upper_tree(counters, n_tiles, ticket, reinterpret_cast<uint32_t *>(ring), &is_last, nb);
 }
 
 // ---------------------------------------------------------------------------

@@ -1778,6 +1778,7 @@ __global__ void k_initialize(const cbtm_pool p, const int32_t *__restrict__ he_n
     }
     if (gid == 0) {
         p.counter[0] = 0;
+        p.counters[0] = 0; // no stamp: the reduction that follows rebuilds every level
         if (p.stats)
             for (int k = 0; k < CBTM_STATS_WORDS; ++k) p.stats[k] = 0;
         if (ctl) {
@@ -1786,7 +1787,8 @@ __global__ void k_initialize(const cbtm_pool p, const int32_t *__restrict__ he_n
             ctl->tail_count = 0;
             ctl->seq_frame = 0;
             ctl->need_total = 0;
-            *ticket = 0;
+            ticket[0] = 0;
+            ticket[1] = 0; // k_sum_reduce's tile claim counter
             for (int k = 0; k < CBTM_STATS_WORDS; ++k) ctl->stats[k] = 0;
         }
     }

@@ -149,3 +149,45 @@ def test_dump_format_and_raw_heap_functions():
     cbt_mod.nb_one_to_bit_ids(nodes, n, ranks, out, 0, ranks.size)
     assert np.array_equal(out, np.flatnonzero(nodes[n:]))
     assert cbt_mod.nb_zero_to_bit_id(nodes, n, 0) == int(np.flatnonzero(nodes[n:] == 0)[0])
+
+
+def test_held_leaf_view_stays_live_like_the_reference():
+    """The reference's ``leaves`` / ``nodes`` are live views of the heap: a caller may keep
+    the array and write it again after a reduction (cbt.py:30-57).  The host mirror must
+    not drop such writes, nor may a refresh from the device overwrite them."""
+    c = Cbt(6)
+    lv = c.leaves
+    lv[3] = 1
+    c.sum_reduce()
+    lv[40] = 1                      # written through the view held across a device operation
+    c.sum_reduce()
+    assert c.count() == 2 and c.one_to_bit_id(1) == 40
+    nd = c.nodes                    # held heap view: internal nodes refresh in place
+    assert nd[1] == 2 and nd[64 + 3] == 1 and nd[64 + 40] == 1
+    lv[41] = 1
+    assert c.get_bit(41) == 1       # a read in between must not lose the write either
+    c.sum_reduce()
+    assert c.count() == 3 and nd[1] == 3 and c.zero_to_bit_id(0) == 0
+    assert [int(x) for x in c.one_to_bit_ids([0, 1, 2])] == [3, 40, 41]
+    lv[3] = 0
+    c.sum_reduce()
+    assert c.count() == 2 and c.one_to_bit_id(0) == 40
+
+
+def test_held_view_of_a_pool_cbt_survives_an_engine_update():
+    """Writes made through a held view after the engine changed the device bitfield are
+    merged into the newer device state, not replaced by it and not replacing it."""
+    from paper_2407_02215_b200 import halfedge
+    from paper_2407_02215_b200.pipeline import ParallelEngine, SplitAll
+    from paper_2407_02215_b200.state import initialize
+    st = initialize(halfedge.single_triangle(), 5)
+    lv = st.cbt.leaves
+    assert int(lv.sum()) == 3
+    with ParallelEngine() as eng:
+        s = eng.update(st, SplitAll())
+    live = s.live_after
+    free = int(np.flatnonzero(st.cbt.nodes[32:] == 0)[-1])
+    lv[free] = 1                    # held view, written after the update
+    st.cbt.sum_reduce()
+    assert st.cbt.count() == live + 1 and st.cbt.get_bit(free) == 1
+    assert int(lv.sum()) == live + 1   # the view shows the device's leaves plus the write
