@@ -98,7 +98,17 @@ enum {
     CBTM_STAT_SEQ = 31,      /* = CBTM_STAT_FRAME, but stored LAST: the other words are written, then a
                               * system-scope fence, then this one -- so when cbtm_pool.stats points to
                               * host-mapped pinned memory the host may poll this word (cbtm_wait_frame)
-                              * and then read the frame's counters without any stream synchronisation */
+                              * and then read the frame's counters without any stream synchronisation.
+                              * cbtm_update publishes the counters of its frame EARLY: as soon as every
+                              * command is final (after stage 5a: admission, split masks, merge agreement
+                              * and allocation counts decide all of them; live_after = live_before -
+                              * freed + allocated), while stages 5b-9 are still running on the stream --
+                              * the host-side work between two frames overlaps with them and the next
+                              * launch is queued behind a running kernel.  Not in that early copy: the
+                              * poison count (0) and the times of phases 4-6 (words 19-21); the complete
+                              * row follows at the end of the frame: */
+    CBTM_STAT_DONE = 30,     /* = CBTM_STAT_FRAME, stored after the frame's reduction and the complete
+                              * row (cbtm_wait_frame_done) */
     /* words 16..21: device time of each phase of the frame in ns (persistent
      * frame kernel only; 0 on the staged path): index (stages 1-3), classify +
      * admission + command scatter (stage 4), merge agreement (stage 5a), slot
@@ -279,6 +289,14 @@ int cbtm_update_finish(const cbtm_pool *pool, const cbtm_verdict *verdict, uintp
  *      ParallelEngine.update (pipeline.py:303-322 reads its counters on the host after every
  *      update).  Returns 0, or CBTM_E_TIMEOUT after timeout_ns. */
 int cbtm_wait_frame(const int64_t *host_stats, int64_t frame, uint64_t timeout_ns);
+/* same for host_stats[CBTM_STAT_DONE]: the frame has finished completely (reduction included) */
+int cbtm_wait_frame_done(const int64_t *host_stats, int64_t frame, uint64_t timeout_ns);
+/* cbtm_update + cbtm_wait_frame in one call (one FFI crossing per frame): launches the frame and
+ * spins until its counters are in host_stats (= the host address of pool->stats, pinned and
+ * device-mapped).  The frame number waited for is host_stats[CBTM_STAT_SEQ] + 1 as read before the
+ * launch.  Returns 0, a contract / CUDA status of the launch, or CBTM_E_TIMEOUT. */
+int cbtm_update_wait(const cbtm_pool *pool, const cbtm_verdict *verdict, const int64_t *host_stats,
+                     uint64_t timeout_ns, uintptr_t stream);
 
 /* ---- the frame loop of a real-time client (cmd_animate, cli.py:226-237: one update per camera,
  *      counters read back every frame) without a kernel launch per frame.  cbtm_update_linger =

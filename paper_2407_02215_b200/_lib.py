@@ -21,6 +21,7 @@ STATS_WORDS = 32
 STAT_PHASE_NS = 16
 STAT_FRAME = 11
 STAT_SEQ = 31
+STAT_DONE = 30
 PHASE_NAMES = ("index", "classify_admit_scatter", "agree", "reserve", "apply", "reduce_publish")
 MIN_DEPTH = 1
 MAX_DEPTH_ABI = 30
@@ -98,6 +99,8 @@ SIGNATURES = {
     "cbtm_post_request": (C.c_int, [_P, _I64, _P]),
     "cbtm_run_epochs": (C.c_int, [C.POINTER(CPool), C.POINTER(CVerdict), C.c_int32, _P, _UP]),
     "cbtm_wait_frame": (C.c_int, [_P, _I64, C.c_uint64]),
+    "cbtm_wait_frame_done": (C.c_int, [_P, _I64, C.c_uint64]),
+    "cbtm_update_wait": (C.c_int, [C.POINTER(CPool), C.POINTER(CVerdict), _P, C.c_uint64, _UP]),
     "cbtm_run_lod_sequence_batch": (C.c_int, [C.POINTER(CPool), C.c_int32, _P, _P, C.c_int32, _P, _UP]),
 }
 

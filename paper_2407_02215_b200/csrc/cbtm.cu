@@ -520,10 +520,10 @@ int cbtm_mesh_from_polygons(const int32_t *face_offsets, const int32_t *face_ver
     return launch_status();
 }
 
-int cbtm_wait_frame(const int64_t *host_stats, int64_t frame, uint64_t timeout_ns)
+static int wait_word(const int64_t *host_stats, int word, int64_t frame, uint64_t timeout_ns)
 {
     if (!host_stats) return CBTM_E_NULL;
-    const volatile int64_t *seq = host_stats + CBTM_STAT_SEQ;
+    const volatile int64_t *seq = host_stats + word;
     if (*seq >= frame) return 0;
     const auto t0 = std::chrono::steady_clock::now();
     for (unsigned spins = 0;; ++spins) {
@@ -535,6 +535,26 @@ int cbtm_wait_frame(const int64_t *host_stats, int64_t frame, uint64_t timeout_n
     }
     std::atomic_thread_fence(std::memory_order_acquire);
     return 0;
+}
+
+int cbtm_wait_frame(const int64_t *host_stats, int64_t frame, uint64_t timeout_ns)
+{
+    return wait_word(host_stats, CBTM_STAT_SEQ, frame, timeout_ns);
+}
+
+int cbtm_wait_frame_done(const int64_t *host_stats, int64_t frame, uint64_t timeout_ns)
+{
+    return wait_word(host_stats, CBTM_STAT_DONE, frame, timeout_ns);
+}
+
+int cbtm_update_wait(const cbtm_pool *pool, const cbtm_verdict *verdict, const int64_t *host_stats,
+                     uint64_t timeout_ns, uintptr_t stream)
+{
+    if (!host_stats) return CBTM_E_NULL;
+    const int64_t frame = *(const volatile int64_t *)(host_stats + CBTM_STAT_SEQ) + 1;
+    const int rc = cbtm_update(pool, verdict, stream);
+    if (rc) return rc;
+    return wait_word(host_stats, CBTM_STAT_SEQ, frame, timeout_ns);
 }
 
 int cbtm_run_epochs(const cbtm_pool *pool, const cbtm_verdict *verdict, int32_t n_frames, int64_t *stats_out,

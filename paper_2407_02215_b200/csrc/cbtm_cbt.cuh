@@ -59,7 +59,7 @@ __device__ __forceinline__ void publish_frame(const ReducePublish &pub, uint32_t
             pub.ctl_stats[tid] = v;
         }
         const int64_t frame = __shfl_sync(FULL_MASK, v, CBTM_STAT_FRAME);
-        if (tid == CBTM_STAT_SEQ) v = frame;
+        if (tid == CBTM_STAT_SEQ || tid == CBTM_STAT_DONE) v = frame;
         if (tid >= CBTM_STAT_PHASE_NS && tid < CBTM_STAT_PHASE_NS + CBTM_STAT_PHASES) {
             v = 0;
             if (pub.phase_t) { // stamp k = start of phase k; the frame ends now
@@ -72,16 +72,58 @@ __device__ __forceinline__ void publish_frame(const ReducePublish &pub, uint32_t
         if (pub.stats_seq) pub.stats_seq[(size_t)CBTM_STATS_WORDS * (*pub.seq_frame) + tid] = v;
         // pool stats may live in host-mapped memory: counters first, fence, sequence word last
         if (pub.pool_stats) { // warp-uniform
-            if (tid != CBTM_STAT_SEQ) pub.pool_stats[tid] = v;
+            if (tid != CBTM_STAT_SEQ && tid != CBTM_STAT_DONE) pub.pool_stats[tid] = v;
             __threadfence_system();
             __syncwarp();
-            if (tid == CBTM_STAT_SEQ) *(volatile int64_t *)&pub.pool_stats[tid] = v;
+            if (tid == CBTM_STAT_SEQ || tid == CBTM_STAT_DONE) *(volatile int64_t *)&pub.pool_stats[tid] = v;
         }
         // the per-frame counters start the next frame at zero
         if (tid < CBTM_STAT_PHASE_NS && tid != CBTM_STAT_FRAME) pub.ctl_stats[tid] = 0;
     }
     __syncwarp();
     if (tid == 0) *pub.seq_frame += 1;
+}
+
+// The counters of a frame as soon as they are DECIDED: after the agreement phase every command
+// is final (admission, split masks, merge agreement, allocation counts), so splits / merges applied,
+// slots allocated and -- from them, pipeline.py:316-322 asserts exactly that identity -- the live
+// count after the frame are known three phases before the frame has been applied and reduced.
+// Written to pool->stats (host-mapped memory in ParallelEngine.update, which returns on the sequence
+// word).  Not in this early row: the poison count of stage 6 (diagnostic, 0 by construction) and the
+// times of the phases that have not run yet.  The frame's bookkeeping (per-frame rows, counter
+// reset, the complete row, CBTM_STAT_DONE) stays with publish_frame at the end of the frame.  One warp.
+__device__ __forceinline__ void publish_early(const int64_t *ctl_stats, int64_t *pool_stats,
+                                              const unsigned long long *phase_t, int tid)
+{
+    if (tid >= CBTM_STATS_WORDS) return;
+    int64_t v = ctl_stats[tid];
+    const bool alloc = tid == CBTM_STAT_SPLIT_ALLOC || tid == CBTM_STAT_MERGE_ALLOC;
+    const bool freed = tid == CBTM_STAT_SPLIT_FREED || tid == CBTM_STAT_MERGE_FREED;
+    int64_t live_after = (tid == CBTM_STAT_LIVE_BEFORE || alloc) ? v : freed ? -v : 0;
+    int64_t allocated = alloc ? v : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        live_after += __shfl_xor_sync(FULL_MASK, live_after, o);
+        allocated += __shfl_xor_sync(FULL_MASK, allocated, o);
+    }
+    if (tid == CBTM_STAT_LIVE_AFTER) v = live_after;
+    if (tid == CBTM_STAT_ALLOCATED) v = allocated;
+    if (tid == CBTM_STAT_POISON) v = 0;
+    if (tid == CBTM_STAT_FRAME) v += 1;
+    const int64_t frame = __shfl_sync(FULL_MASK, v, CBTM_STAT_FRAME);
+    if (tid >= CBTM_STAT_PHASE_NS && tid < CBTM_STAT_PHASE_NS + CBTM_STAT_PHASES) {
+        const int k = tid - CBTM_STAT_PHASE_NS;
+        v = 0;
+        if (phase_t && k < 3) { // index, classify, agree have run
+            const unsigned long long t0 = phase_t[k];
+            const unsigned long long t1 = k < 2 ? phase_t[k + 1] : global_ns();
+            v = t1 > t0 ? (int64_t)(t1 - t0) : 0;
+        }
+    }
+    if (tid != CBTM_STAT_SEQ && tid != CBTM_STAT_DONE) pool_stats[tid] = v;
+    __threadfence_system();
+    __syncwarp();
+    if (tid == CBTM_STAT_SEQ) *(volatile int64_t *)&pool_stats[tid] = frame;
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)

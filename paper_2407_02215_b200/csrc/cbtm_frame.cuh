@@ -775,9 +775,15 @@ __device__ __forceinline__ void phase_scatter(const FrameArgs &a, uint32_t bid, 
 __device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb)
 {
     __shared__ uint32_t wsum[CHUNK / 32];
+    __shared__ uint32_t acc[4];
     const cbtm_pool &p = a.pool;
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // The frame's counters (kernels.py:609-632 counts them in stage 8) are decided here: who is
+    // consumed by a split, who by an agreed merge, how many slots each allocates.  Counting them
+    // now lets the frame publish its UpdateStats two phases before it has been applied.
+    uint32_t split_freed = 0, merge_freed = 0, split_alloc = 0, merge_alloc = 0;
+    if (tid < 4) acc[tid] = 0; // (ordered before the atomics below by the barriers of the chunk loop / the one after it)
     for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
         const uint32_t i = chunk * CHUNK + tid;
         uint32_t na = 0;
@@ -792,6 +798,8 @@ __device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t n, uint
             int32_t ref = -1;
             if (sm) {
                 na = 2 + ((sm >> 1) & 1) + ((sm >> 2) & 1);
+                ++split_freed;
+                split_alloc += na;
             } else if (cmd & CBTM_CMD_MERGE) {
                 const MergeCfg c = merge_config_admitted(js, nx, pv, cmd, j4_hint);
                 // one round trip: the members' command words and ids
@@ -814,6 +822,8 @@ __device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t n, uint
                     if (j4 < best) best = j4, owner = c.j4;
                     ref = 2 * owner + ((c.kind == 2 && (js >> 1) != (best >> 1)) ? 1 : 0);
                     if (cmd & CBTM_CMD_OWNER) na = (cmd & CBTM_CMD_QUAD) ? 2 : 1;
+                    ++merge_freed; // every member of an agreed merge is consumed; the owner allocates
+                    merge_alloc += na;
                 }
             }
             a.ws.merge_ref[s] = ref;
@@ -830,6 +840,19 @@ __device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t n, uint
         }
         __syncthreads();
     }
+    __syncthreads();
+    // one atomic per counter and warp in shared memory, one per counter and CTA in global memory
+    const uint32_t w_sf = warp_sum(split_freed), w_mf = warp_sum(merge_freed);
+    const uint32_t w_sa = warp_sum(split_alloc), w_ma = warp_sum(merge_alloc);
+    if (lane == 0) {
+        if (w_sf) atomicAdd(&acc[0], w_sf);
+        if (w_mf) atomicAdd(&acc[1], w_mf);
+        if (w_sa) atomicAdd(&acc[2], w_sa);
+        if (w_ma) atomicAdd(&acc[3], w_ma);
+    }
+    __syncthreads();
+    if (tid < 4 && acc[tid])
+        atomicAdd((unsigned long long *)&a.ws.ctl->stats[CBTM_STAT_SPLIT_FREED + tid], (unsigned long long)acc[tid]);
 }
 
 // sum of v[lo, hi) by the whole CTA (every thread gets it); scratch: CHUNK / 32 words
@@ -1285,14 +1308,13 @@ __device__ __forceinline__ void apply_merged_pair(ApplyCtx &cx, int32_t e, int32
 
 __device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb)
 {
-    __shared__ uint32_t acc[5];
+    __shared__ uint32_t poisoned;
     const cbtm_pool &p = a.pool;
     const uint32_t nch = (n + CHUNK - 1) / CHUNK;
     const int tid = threadIdx.x;
-    if (tid < 5) acc[tid] = 0;
+    if (tid == 0) poisoned = 0;
     __syncthreads();
     ApplyCtx cx{p, a.ws.merge_ref, a.ws.dirty, 0};
-    uint32_t split_freed = 0, merge_freed = 0, split_alloc = 0, merge_alloc = 0;
     const BitSink bits32{reinterpret_cast<uint32_t *>(p.bits), cx.dirty};
 
     for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
@@ -1309,19 +1331,13 @@ __device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t n, uint
         const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
         if (na == 0) {
             // not allocating: either untouched, or a non-owner member of an agreed merge
-            if (!sm && mref >= 0) {
-                set_free(bits32, s);
-                ++merge_freed;
-            }
+            if (!sm && mref >= 0) set_free(bits32, s);
             continue;
         }
         if (sm) {
             apply_split(cx, s, sm, own);
-            ++split_freed;
-            split_alloc += 2 + ((sm >> 1) & 1) + ((sm >> 2) & 1);
         } else { // owner of an agreed merge: kernels.py:464-491, 562-594, 624-628
             set_free(bits32, s);
-            ++merge_freed;
             const uint64_t js = own.id;
             const MergeCfg c = merge_config_admitted(js, own.nx, own.pv, cmd, j4_hint);
             const bool quad = c.kind == 2;
@@ -1358,24 +1374,17 @@ __device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t n, uint
                 apply_merged_pair(cx, e2, o2, id_e2, p2, p1, n2, q2);
                 set_live(bits32, p1);
                 set_live(bits32, p2);
-                merge_alloc += 2;
             } else {
                 apply_merged_pair(cx, e1, o1, id_e1, p1, -1, n1, q1);
                 set_live(bits32, p1);
-                merge_alloc += 1;
             }
         }
     }
-    if (split_freed) atomicAdd(&acc[0], split_freed);
-    if (merge_freed) atomicAdd(&acc[1], merge_freed);
-    if (split_alloc) atomicAdd(&acc[2], split_alloc);
-    if (merge_alloc) atomicAdd(&acc[3], merge_alloc);
-    if (cx.poison) atomicAdd(&acc[4], cx.poison);
+    // (the frame's counters were taken in phase_agree; what is left to report is the poison count)
+    if (cx.poison) atomicAdd(&poisoned, cx.poison);
     __syncthreads();
-    if (tid < 5 && acc[tid]) {
-        const int slot = tid < 4 ? CBTM_STAT_SPLIT_FREED + tid : CBTM_STAT_POISON;
-        atomicAdd((unsigned long long *)&a.ws.ctl->stats[slot], (unsigned long long)acc[tid]);
-    }
+    if (tid == 0 && poisoned)
+        atomicAdd((unsigned long long *)&a.ws.ctl->stats[CBTM_STAT_POISON], (unsigned long long)poisoned);
 }
 
 // ---------------------------------------------------------------------------
@@ -1497,6 +1506,14 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         WORK_END(ctl, 2);
         grid.sync();
         if (stamp) stamp[3] = global_ns();
+        // The launch's last frame: every counter of the frame is decided (admission, agreement,
+        // allocation counts), so they go to the host NOW, three phases before the frame is done --
+        // ParallelEngine.update returns on them and the host's work between two frames (stats
+        // object, next camera, next launch call) overlaps with reserve / apply / reduce instead of
+        // following them; the next launch is queued while this one still runs.  The CTA with the
+        // fewest chunks does it (none at all for up to 75 k live bisectors).
+        if (bid == nb - 1 && !mailbox && f == n_frames - 1 && p.stats)
+            publish_early(ctl->stats, p.stats, ctl->phase_t[f & 1], threadIdx.x);
         phase_reserve(a, n, bid, nb);
         WORK_END(ctl, 3);
         grid.sync();

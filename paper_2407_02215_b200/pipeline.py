@@ -84,6 +84,14 @@ class UpdateStats:
 _N_PHASES = len(_lib.PHASE_NAMES)
 
 
+def _checked(stats: UpdateStats) -> UpdateStats:
+    # pipeline.py:316-322 of the reference
+    assert stats.live_after == (stats.live_before - stats.splits_applied + stats.split_allocs
+                                - stats.merges_applied + stats.merge_allocs), \
+        "live count does not match applied operations"
+    return stats
+
+
 def write_stats_csv(stats_list, no_timing: bool = False) -> str:
     buf = io.StringIO()
     buf.write(CSV_HEADER + "\n")
@@ -239,11 +247,29 @@ class ParallelEngine:
 
     def update(self, state: TriangulationState, decide, epoch: int = 0) -> UpdateStats:
         """One full nine-stage update; returns its counters.  The frame kernel
-        writes them into host-mapped memory; waiting for their sequence word is
-        the only synchronisation (no copy, no stream synchronise)."""
+        writes them into host-mapped memory as soon as they are decided (after
+        stage 5a: admission, merge agreement and allocation counts fix every
+        counter) and this call returns on their sequence word: no copy, no
+        stream synchronise, and stages 5b-9 are still draining on the state's
+        stream while the caller prepares the next frame (everything that
+        touches the state is ordered behind them on that stream).  The early
+        row carries no poison count and no times for the phases still running;
+        ``profile=True`` waits for the complete frame instead."""
         L = _lib.load()
         # the reference reads cbt.count() first, which asserts a reduced tree (pipeline.py:211, cbt.py:70-73)
         assert not state.cbt._dirty, "sum_reduce required before count()"
+        cv = decide.device_verdict(state) if isinstance(decide, KernelDecide) else None
+        if cv is not None and not self.profile and not (self.linger_ns and cv.mode == _lib.VERDICT_LOD):
+            # device verdict source: stages 1-9 in one cooperative launch; launch + wait for the
+            # frame's counters in ONE call into the library
+            rc = L.cbtm_update_wait(state.c_pool_ref(), cv, state._stats_host_ptr, 20_000_000_000,
+                                    state.stream())
+            if rc:
+                if rc == 7:
+                    state.synchronize()  # surfaces a CUDA error if the frame kernel died
+                _lib.check(rc, "cbtm_update_wait")
+            state._touched()
+            return _checked(UpdateStats.from_device_words(state._stats_np.tolist(), epoch))
         pool = state.c_pool()
         stream = state.stream()
         seq_before = int(state._stats_np[_lib.STAT_SEQ])
@@ -252,15 +278,11 @@ class ParallelEngine:
             t = _lib.torch()
             events = [t.cuda.Event(enable_timing=True) for _ in range(3)]
             events[0].record()
-        cv = decide.device_verdict(state) if isinstance(decide, KernelDecide) else None
         keep_alive = None
         lingering = False
-        if cv is not None and not events and self.linger_ns and cv.mode == _lib.VERDICT_LOD:
+        if cv is not None and not events:
             lingering = True
             self._update_linger(state, pool, cv, stream, seq_before)
-        elif cv is not None and not events:
-            # device verdict source: stages 1-9 in one call (one cooperative launch)
-            _lib.check(L.cbtm_update(C.byref(pool), C.byref(cv), stream), "cbtm_update")
         else:
             _lib.check(L.cbtm_update_begin(C.byref(pool), stream), "cbtm_update_begin")
             state._version += 1  # cache_live changed
@@ -278,7 +300,8 @@ class ParallelEngine:
             if events:
                 events[2].record()
         if not lingering:
-            rc = L.cbtm_wait_frame(state._stats_host_ptr, seq_before + 1, 20_000_000_000)
+            wait = L.cbtm_wait_frame_done if events else L.cbtm_wait_frame
+            rc = wait(state._stats_host_ptr, seq_before + 1, 20_000_000_000)
             if rc:
                 state.synchronize()  # surfaces a CUDA error if the frame kernel died
                 _lib.check(rc, "cbtm_wait_frame")
@@ -292,12 +315,7 @@ class ParallelEngine:
             times = [0] * 9
             times[1] = int(events[0].elapsed_time(events[1]) * 1000)
             times[3] = int(events[1].elapsed_time(events[2]) * 1000)
-        stats = UpdateStats.from_device_words(words, epoch, times)
-        assert stats.live_after == (stats.live_before - stats.splits_applied
-                                    + stats.split_allocs - stats.merges_applied
-                                    + stats.merge_allocs), \
-            "live count does not match applied operations"
-        return stats
+        return _checked(UpdateStats.from_device_words(words, epoch, times))
 
     def _update_linger(self, state, pool, cv, stream, seq_before) -> None:
         """One LOD frame through the lingering frame kernel: posted to the

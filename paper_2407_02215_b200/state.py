@@ -137,6 +137,15 @@ class TriangulationState:
         self._c_pool = (key, pool)
         return pool
 
+    def c_pool_ref(self):
+        """ctypes reference to :meth:`c_pool` (cached with it): the per-frame path passes the
+        same object every frame."""
+        pool = self.c_pool()
+        ref = getattr(self, "_c_pool_ref", None)
+        if ref is None or ref[0] is not pool:
+            self._c_pool_ref = ref = (pool, C.byref(pool))
+        return ref[1]
+
     def _build_c_pool(self, wide: bool = False) -> _lib.CPool:
         p = _lib.ptr
         return _lib.CPool(
