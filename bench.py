@@ -1,37 +1,49 @@
 #!/usr/bin/env python
 """bench.py -- per-frame bisector update on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload earth|batch]
 
 A *step* is one full nine-stage update (index + classify + admit + split/merge +
-bitfield + sum reduction) of one planet for one camera frame.  The workload at
-N = 1 is BASELINE config 3: the Earth-scale icosphere planet on a 2^26-slot pool,
-LOD camera sweeping between the ground (10 m) and space (3 R).  Untimed setup
-flies the camera down to the ground (64 frames); the warm-up and timed steps then
-ride the ground<->space sweep (period 128 frames), so the pool keeps splitting
-and merging for any K.  With N > 1 every rank owns one such planet (camera path
-rotated by rank * 45 degrees, as BASELINE config 5 rotates its planets): weak
-scaling, no data-path collective, one final gather of the per-rank stats.
+bitfield + sum reduction) for one camera frame.
+
+workload `earth` (default at N = 1): BASELINE config 3, ONE Earth-scale icosphere planet
+  on a 2^26-slot pool, LOD camera sweeping between the ground (10 m) and space (3 R).
+  Untimed setup flies the camera down to the ground (64 frames); the warm-up and timed
+  steps ride the ground<->space sweep (period 128 frames), so the pool keeps splitting
+  and merging for any K.
+workload `batch` (default at N > 1): BASELINE config 5, EIGHT independent icosphere
+  planets on 2^24-slot pools (paths rotated by p * 45 degrees), planet p on rank p mod N
+  (`batch.run_planet_batch`); a step advances every planet by one frame; the planets of a
+  rank run in lockstep inside one launch; no data-path collective, one final all_gather
+  of the per-frame stats (NCCL).  Total work is fixed: strong scaling.
+`--gpus N` without a torchrun environment re-executes itself under
+`python -m torch.distributed.run --nproc-per-node N` (one rank per GPU).
 
 Reported on ONE JSON line (rank 0):
-  value / ms_per_step  device-timed (CUDA events on the launch stream) K-step run
-                       through cbtm_run_lod_sequence, camera parameters already
-                       resident in HBM, no host synchronisation between frames
-  e2e                  the same K frames through the public python API
-                       (ParallelEngine.update + LodDecide per frame): per-frame
-                       host->device camera parameters and device->host stats read
-  roofline             the persistent frame kernel k_frames (the only kernel of the
+  value / ms_per_step  device-timed (CUDA events on the launch stream) K-step run with the
+                       camera parameters already resident in HBM, no host synchronisation
+                       between frames
+  e2e                  the same K frames through the public python API with host inputs:
+                       earth: `ParallelEngine().update(state, LodDecide(config, camera, mesh))`
+                       per frame (default engine, nothing subtracted: the clock runs from
+                       before the first update until the stream has drained after the last);
+                       batch: `pipeline.run_lod_sequence_batch` (parameters uploaded, stats
+                       downloaded inside the timed region)
+  roofline             earth: the persistent frame kernel k_frames (the only kernel of the
                        timed region) against the HBM roofline, algorithmic bytes as
-                       SURVEY.md 8(d) defines them; cbt_kernels_d26 / config4_d30 time
-                       the two full-pool CBT kernels (sum reduction, decode-all) alone,
-                       on the pool's own bitfield and at 2^30 leaves where they are
-                       HBM bound
-  cpu_baseline         the oracle port of the reference CPU path on this box's
-                       host cores, on a bounded sample of the same frames, started
-                       from the same pool state (also a parity check of the run)
+                       SURVEY.md 8(d) defines them; `traffic` from the ncu capture recorded in
+                       profiles/kframes_traffic.json.  cbt_kernels_d26 / config4 time the
+                       full-pool CBT kernels (sum reduction, decode-all) alone, where they
+                       are HBM bound, next to the CPU port on the same bitfield
+  cpu_baseline         the REAL reference (`cbtmesh` from baseline/_ref, all host threads)
+                       on a bounded sample of the same frames, from the same pool state
+                       (kind "reference"); `cpu_port` = the C/OpenMP port of the reference
+                       path (oracle/) on more frames; `cpu_reference` = the reference at
+                       1 thread and all threads, also on BASELINE config 2
 
---impl reference runs the reference's CPU algorithm (oracle port, all host
-threads) on the same workload: CPU only, none of the CUDA code.
+--impl reference runs the reference's CPU implementation of the path on the same workload:
+the real `cbtmesh.pipeline.ParallelEngine(threads=cpu_count)` when baseline/_ref is present
+(kind "reference"), else the C port (kind "port").  CPU only, none of the CUDA code.
 """
 
 from __future__ import annotations
@@ -39,6 +51,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -50,14 +63,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "update ms/frame & bisectors/s (classify+split/merge+CBT reduce+index)"
-# dram__bytes_read.sum + dram__bytes_write.sum of k_frames per frame, from the committed ncu capture
-KFRAMES_DRAM_BYTES_PER_FRAME = {26: 1410560}  # (4 229 376 + 2 304) / 3 frames
 UNIT = "bisectors/s"
 SETUP_FRAMES = 64
+BATCH_PLANETS = 8
+BATCH_DEPTH = 24
+DTYPE = "int32/u64 + f64 classifier"
 
 
 def sweep_params(depth: int, rotate_deg: float):
-    """(mesh, config, descent prm[64,23], cyclic sweep prm[128,23])."""
+    """(sequence, descent prm[64,23], cyclic sweep prm[128,23])."""
     from paper_2407_02215_b200 import workloads
     seq = workloads.earth_sweep(depth=depth, frames=SETUP_FRAMES, rotate_deg=rotate_deg)
     prm = seq.params()
@@ -71,12 +85,32 @@ def step_params(cycle: np.ndarray, first: int, count: int) -> np.ndarray:
     return np.ascontiguousarray(cycle[idx])
 
 
+def step_cameras(seq, first: int, count: int) -> list:
+    cams = seq.cameras
+    cam_cycle = cams[SETUP_FRAMES - 1::-1] + cams[:SETUP_FRAMES]
+    return [cam_cycle[(first + j) % len(cam_cycle)] for j in range(count)]
+
+
 def load_peaks() -> tuple[float, str]:
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         with open(path) as fh:
             return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
     return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(depth: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum of k_frames per frame, from the ncu
+    capture recorded (with the commit it was taken at) in profiles/kframes_traffic.json."""
+    path = os.path.join(ROOT, "profiles", "kframes_traffic.json")
+    try:
+        with open(path) as fh:
+            rec = json.load(fh)
+        row = rec["pools"][str(depth)]
+        return row["dram_bytes_per_frame"], (f"{rec['source']} at commit {rec['commit']}: "
+                                             f"{row['note']}")
+    except (OSError, KeyError, ValueError):
+        return None, "no ncu capture on record for this pool depth (profiles/kframes_traffic.json)"
 
 
 class ClockSampler:
@@ -133,7 +167,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU arms (oracle port of the reference path)
+# CPU arms: the real reference (baseline/_ref) and the C port (oracle/)
 # ---------------------------------------------------------------------------
 
 def oracle_pool_from_host(mesh, depth, host_arrays):
@@ -144,8 +178,8 @@ def oracle_pool_from_host(mesh, depth, host_arrays):
     return op
 
 
-def cpu_sample(op, mesh, prms, threads):
-    """Time len(prms) genuine oracle frames; returns (seconds, stats rows)."""
+def port_sample(op, mesh, prms, threads):
+    """Time len(prms) genuine frames of the C port; returns (seconds, stats rows)."""
     from oracle import OracleVerdict
     rows, total = [], 0.0
     for prm in prms:
@@ -156,46 +190,103 @@ def cpu_sample(op, mesh, prms, threads):
     return total, rows
 
 
+def reference_available() -> bool:
+    from baseline import ref_timing
+    return ref_timing.available()
+
+
+def host_arrays_of_oracle(op) -> dict:
+    return {k: getattr(op, k) for k in ("ids", "nexts", "prevs", "twins", "commands", "reserved", "counter",
+                                        "cache_live", "cache_free", "nodes")}
+
+
+def workload_config(args, n_gpus, workload):
+    if workload == "batch":
+        return {"workload": f"planet_batch: {BATCH_PLANETS} icosphere planets (H=240), pools 2^{BATCH_DEPTH} slots, camera "
+                            f"paths rotated by p*45 deg, LOD camera ground(10 m)<->space(3R) sweep 1920x1080, 49 px target; "
+                            f"{SETUP_FRAMES} untimed descent frames then steps ride the 128-frame cycle",
+                "pool_depth": BATCH_DEPTH, "planets": BATCH_PLANETS,
+                "parallelism": f"planet p on rank p mod {n_gpus} (round robin), the planets of a rank in lockstep in one "
+                               "launch, no collective on the data path, one final all_gather of the stats",
+                "l2": "pool state (8 x 0.83 GB) exceeds L2"}
+    return {"workload": f"earth_sweep icosphere H=240, pool 2^{args.depth} slots, LOD camera "
+                        f"ground(10 m)<->space(3R) sweep 1920x1080, 49 px target; "
+                        f"{SETUP_FRAMES} untimed descent frames then steps ride the 128-frame cycle",
+            "pool_depth": args.depth, "planets": n_gpus,
+            "parallelism": "1 planet per GPU, no collective on the data path",
+            "l2": "pool state (3.3 GB) exceeds L2; roofline kernels timed with L2 flushed"}
+
+
 def run_reference(args):
-    """--impl reference: the reference CPU algorithm (oracle port), CPU only."""
+    """--impl reference: the reference's CPU implementation of the path, CPU only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import oracle
     from oracle import OraclePool, OracleVerdict
     threads = oracle.max_threads()
-    seq, down, cycle = sweep_params(args.depth, 0.0)
-    op = OraclePool(seq.mesh, args.depth)
-    for prm in down:  # untimed setup: fast-forward with the linear-scan stage 2
-        op.update(OracleVerdict.lod(seq.mesh, prm), threads=threads, fast_setup=True)
-    for prm in step_params(cycle, 0, args.warmup):
-        op.update(OracleVerdict.lod(seq.mesh, prm), threads=threads)
-    seconds, rows = cpu_sample(op, seq.mesh, step_params(cycle, args.warmup, args.steps), threads)
-    units = sum(r[6] for r in rows)
-    value = units / seconds
+    workload = resolve_workload(args, int(os.environ.get("WORLD_SIZE", str(args.gpus))))
+    depth = BATCH_DEPTH if workload == "batch" else args.depth
+    planets = range(BATCH_PLANETS) if workload == "batch" else range(1)
+    use_ref = reference_available() and not args.port_only
+    if use_ref:
+        from baseline import ref_timing
+        ref_timing.load()
+        jit_s = ref_timing.warm_jit(threads)
+    seconds, units, port_seconds, port_units = 0.0, 0, 0.0, 0
+    W, K = args.warmup, args.steps
+    for p in planets:
+        seq, down, cycle = sweep_params(depth, 45.0 * p)
+        op = OraclePool(seq.mesh, depth)
+        for prm in down:  # untimed setup: fast-forward with the port (linear-scan stage 2)
+            op.update(OracleVerdict.lod(seq.mesh, prm), threads=threads, fast_setup=True)
+        for prm in step_params(cycle, 0, W):
+            op.update(OracleVerdict.lod(seq.mesh, prm), threads=threads, fast_setup=True)
+        timed = step_params(cycle, W, K)
+        if use_ref:
+            st = ref_timing.state_from_arrays(seq.mesh, depth, host_arrays_of_oracle(op))
+            # one untimed frame on a scratch copy is not affordable at 2^26 (3.5 GB): the JIT is warm, the
+            # first timed frame pays only the page faults of the fresh state
+            per_frame, ref_rows = ref_timing.time_frames(st, seq.mesh, seq.config, step_cameras(seq, W, K), threads)
+            seconds += sum(per_frame)
+            units += sum(r[6] for r in ref_rows)
+            del st
+        n_port = K if not use_ref else min(K, 4)
+        sec, rows = port_sample(op, seq.mesh, timed[:n_port], threads)
+        # (under reservation pressure the reference at threads > 1 admits in scheduler order --
+        #  pipeline.py:7-9 -- so counters are only comparable on frames without rejections)
+        pressure = any(r[0] or r[1] for r in rows + (ref_rows[:n_port] if use_ref else []))
+        if use_ref and not pressure and rows != ref_rows[:n_port]:
+            raise SystemExit("bench.py: the C port and the real reference disagree on the timed frames")
+        port_seconds += sec
+        port_units += sum(r[6] for r in rows)
+        del op
+    port = {"value": port_units / port_seconds, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": "the C/OpenMP port of the reference path (oracle/) on the first timed frames of every planet"}
+    if use_ref:
+        value = units / seconds
+        cpu = {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+               "sample": f"{K} full frames per planet through the unmodified cbtmesh.pipeline.ParallelEngine(threads={threads})"
+                         f".update + LodDecide (baseline/_ref), numba kernels JIT-warmed first ({jit_s:.0f} s, untimed); "
+                         "setup and warm-up frames fast-forwarded with the C port (identical state, verified on the "
+                         "timed frames)",
+               "port": port}
+    else:
+        value, seconds = port["value"], port_seconds
+        cpu = dict(port, sample=f"{K} full frames per planet (C/OpenMP port of the reference path: baseline/_ref absent)")
+    steps_total = K * len(planets) if workload == "batch" else K
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * seconds / max(1, args.steps), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32/u64 + f64 classifier",
-        "data": "synthetic", "config": workload_config(args, 1),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} full frames of the workload (oracle port of the "
-                                   "reference path, OpenMP over stage 2 / classifier / stage 9)"},
+        "n_gpus": args.gpus, "steps": K, "warmup": W,
+        "ms_per_step": 1e3 * seconds / max(1, K), "higher_is_better": True,
+        "scaling": "strong" if workload == "batch" else "weak", "vs_baseline": None, "dtype": DTYPE,
+        "data": "synthetic", "config": workload_config(args, 1 if workload == "earth" else args.gpus, workload),
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "gpu_launches": 0,
+        "gpu_launches": 0, "frames_timed": steps_total,
     }
     print(json.dumps(line))
     return 0
-
-
-def workload_config(args, n_gpus):
-    return {"workload": f"earth_sweep icosphere H=240, pool 2^{args.depth} slots, LOD camera "
-                        f"ground(10 m)<->space(3R) sweep 1920x1080, 49 px target; "
-                        f"{SETUP_FRAMES} untimed descent frames then steps ride the 128-frame cycle",
-            "pool_depth": args.depth, "planets": n_gpus,
-            "parallelism": "1 planet per GPU, no collective on the data path",
-            "l2": "pool state (3.3 GB) exceeds L2; roofline kernel timed with L2 flushed"}
 
 
 # ---------------------------------------------------------------------------
@@ -208,134 +299,162 @@ def _clean_l2_flush(torch, flush):
     flush.view(torch.int64).sum()
 
 
-def _time_batched(torch, device, flush, launch, copies, reps=15):
-    """Median ms per launch of `launch(k)`, k = 0..copies-1 back to back between
-    one CUDA-event pair, each k on its own cold copy of the data (amortises the
-    ~5 us floor of an event-timed single short launch on this system)."""
-    for k in range(copies):
-        launch(k)
+def _time_graph(torch, device, flush, launch, copies, reps=15):
+    """Median ms per launch of `launch(k, stream)`, k = 0..copies-1, captured as ONE CUDA graph
+    (programmatic-dependent-launch edges included) and replayed between a CUDA-event pair: every
+    k works on its own cold copy of the data, the GPU runs the launches back to back and the
+    host's per-call cost is out of the picture.  L2 flushed by reads before every replay."""
+    side = torch.cuda.Stream(device=device)
+    with torch.cuda.stream(side):
+        for k in range(copies):
+            launch(k, side.cuda_stream)
+    torch.cuda.synchronize(device)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side):
+        for k in range(copies):
+            launch(k, torch.cuda.current_stream(device).cuda_stream)
+    torch.cuda.synchronize(device)
     samples = []
-    for _ in range(reps):
+    for _ in range(reps + 2):
         _clean_l2_flush(torch, flush)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        for k in range(copies):
-            launch(k)
+        graph.replay()
         b.record()
         torch.cuda.synchronize(device)
         samples.append(a.elapsed_time(b) / copies)
-    return float(np.median(samples))
+    return float(np.median(samples[2:]))
 
 
-def reduce_roofline(L, _lib, torch, device, d_bits, depth, peak, peak_src):
-    """k_sum_reduce on the benchmark pool's own bitfield: cold (L2 flushed, HBM
-    bound) and warm (bitfield L2 resident, as inside a frame)."""
+def _time_single(torch, device, flush, launch, reps=7):
+    samples = []
     stream = torch.cuda.current_stream(device).cuda_stream
-    flush = torch.zeros(512 << 20, dtype=torch.uint8, device=device)
-    copies = 8
-    bits = [d_bits.clone() for _ in range(copies)]
-    cnts = [torch.zeros(L.cbtm_counter_words(depth), dtype=torch.int32, device=device) for _ in range(copies)]
-    ws = torch.zeros(1024, dtype=torch.uint8, device=device)
-
-    def launch(k):
-        rc = L.cbtm_sum_reduce(bits[k].data_ptr(), cnts[k].data_ptr(), depth, ws.data_ptr(), 1024, stream)
-        assert rc == 0
-
-    cold_ms = _time_batched(torch, device, flush, launch, copies)
-    # warm: same buffer every launch, no flush (the in-frame regime at D = 26: 8 MB sits in L2)
-    for _ in range(3):
-        launch(0)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(64):
-        launch(0)
-    b.record()
-    torch.cuda.synchronize(device)
-    warm_ms = a.elapsed_time(b) / 64
-    nbytes = (1 << depth) // 8 + 4 * L.cbtm_counter_words(depth)
-    achieved = nbytes / (cold_ms * 1e-3) / 1e9
-    return {"bound": "hbm", "kernel": "k_sum_reduce", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "algorithmic_bytes": nbytes, "kernel_ms": cold_ms, "kernel_ms_warm": warm_ms,
-            "timing": f"CUDA events, {copies} back-to-back launches on {copies} cold copies, L2 flushed by reads, median of 15",
-            "peak_source": peak_src,
-            "note": "standalone full reduction (cbtm_sum_reduce; initialize / Cbt.sum_reduce -- no longer part of a "
-                    "frame): N/8 bitfield bytes read + 4*(2<<Lc) counter bytes written per launch; at 8.9 MB it is "
-                    "fixed-cost bound (launch + ~4 dependent round trips), see config4_d30 for the HBM-bound size"}
+    for _ in range(reps + 1):
+        _clean_l2_flush(torch, flush)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        launch(0, stream)
+        b.record()
+        torch.cuda.synchronize(device)
+        samples.append(a.elapsed_time(b))
+    return float(np.median(samples[1:]))
 
 
-def config4_probe(L, _lib, torch, device, peak):
-    """BASELINE config 4 at its largest size (2^30 leaves, occupancy 0.5): the
-    two full-pool kernels against the HBM roofline, measured live."""
-    depth = 30
+def cbt_kernel_probe(L, torch, device, depth, bits, peak, cpu_pool=None, cpu_threads=1):
+    """The two full-pool CBT kernels of BASELINE config 4 on the given bitfield, cold, against the
+    HBM roofline: k_sum_reduce (graph-batched, per launch) and k_index with both lists (decode-all).
+    With `cpu_pool` (an OraclePool of the same depth) the C port runs the same two operations on
+    the same bits (reference layout: uint32[2N] heap, one root-to-leaf descent per rank)."""
     n = 1 << depth
-    stream = torch.cuda.current_stream(device).cuda_stream
     flush = torch.zeros(512 << 20, dtype=torch.uint8, device=device)
-    gen = torch.Generator(device=device)
-    gen.manual_seed(30050)
-    copies = 4
-    bits = [torch.randint(-2 ** 63, 2 ** 63 - 1, (n // 64,), dtype=torch.int64, device=device, generator=gen)]
-    bits += [bits[0].clone() for _ in range(copies - 1)]
+    copies = 8 if depth <= 28 else 4
+    bits_k = [bits] + [bits.clone() for _ in range(copies - 1)]
     cnts = [torch.zeros(L.cbtm_counter_words(depth), dtype=torch.int32, device=device) for _ in range(copies)]
     ws = torch.zeros(1024, dtype=torch.uint8, device=device)
 
-    def reduce(k):
-        assert L.cbtm_sum_reduce(bits[k].data_ptr(), cnts[k].data_ptr(), depth, ws.data_ptr(), 1024, stream) == 0
+    def reduce(k, stream):
+        assert L.cbtm_sum_reduce(bits_k[k].data_ptr(), cnts[k].data_ptr(), depth, ws.data_ptr(), 1024, stream) == 0
 
-    red_ms = _time_batched(torch, device, flush, reduce, copies, reps=10)
+    red_ms = _time_graph(torch, device, flush, reduce, copies)
+    red_single_ms = _time_single(torch, device, flush, reduce)
     ones = int(cnts[0][1].item())
     live = torch.empty(n, dtype=torch.int32, device=device)
     free = torch.empty(n, dtype=torch.int32, device=device)
 
-    def index(k):
-        assert L.cbtm_index(bits[0].data_ptr(), cnts[0].data_ptr(), depth, live.data_ptr(), free.data_ptr(), 0, stream) == 0
+    def index(k, stream):
+        assert L.cbtm_index(bits.data_ptr(), cnts[0].data_ptr(), depth, live.data_ptr(), free.data_ptr(), 0, stream) == 0
 
-    idx_ms = _time_batched(torch, device, flush, index, 1, reps=5)
+    idx_ms = _time_single(torch, device, flush, index, reps=5)
     # spot check: the compacted lists are sorted and partition the pool
     assert bool((live[1:ones] > live[:ones - 1]).all()) and bool((free[1:n - ones] > free[:n - ones - 1]).all())
     red_bytes = n // 8 + 4 * L.cbtm_counter_words(depth)
     all_bytes = n // 8 + 4 * n
     out = {"leaves": n, "occupancy": ones / n,
            "reduce": {"us": red_ms * 1e3, "GB/s": red_bytes / red_ms / 1e6, "frac": red_bytes / red_ms / 1e6 / peak,
-                      "algorithmic_bytes": red_bytes},
+                      "algorithmic_bytes": red_bytes, "single_launch_us": red_single_ms * 1e3,
+                      "timing": f"{copies} launches on {copies} cold copies as one CUDA graph, per launch, median of 15"},
            "decode_all": {"us": idx_ms * 1e3, "GB/s": all_bytes / idx_ms / 1e6,
-                          "frac": all_bytes / idx_ms / 1e6 / peak, "algorithmic_bytes": all_bytes}}
-    del bits, cnts, live, free
+                          "frac": all_bytes / idx_ms / 1e6 / peak, "algorithmic_bytes": all_bytes,
+                          "timing": "single launch, CUDA events, median of 5"}}
+    if cpu_pool is not None:
+        import ctypes as C
+        import oracle
+        host_bits = bits.cpu().numpy().view(np.uint8)
+        cpu_pool.nodes[n:] = np.unpackbits(host_bits, bitorder="little")[:n]
+        t0 = time.perf_counter()
+        oracle.sum_reduce_nodes(cpu_pool.nodes, depth, cpu_threads)
+        t_red = time.perf_counter() - t0
+        assert int(cpu_pool.nodes[1]) == ones
+        t0 = time.perf_counter()
+        oracle.lib().orc_cache_pointers(C.byref(cpu_pool._cpool()), ones, n - ones, 0, max(ones, n - ones), cpu_threads)
+        t_idx = time.perf_counter() - t0
+        same = (np.array_equal(cpu_pool.cache_live[:ones], live[:ones].cpu().numpy())
+                and np.array_equal(cpu_pool.cache_free[:n - ones], free[:n - ones].cpu().numpy()))
+        if not same:
+            raise SystemExit("bench.py: decode-all on the GPU and on the CPU port disagree")
+        out["cpu_port"] = {"cores": cpu_threads, "reduce_ms": t_red * 1e3, "decode_all_ms": t_idx * 1e3,
+                           "reduce_speedup": t_red / (red_ms * 1e-3), "decode_all_speedup": t_idx / (idx_ms * 1e-3),
+                           "layout": "reference heap uint32[2N] (8 B/slot): sum_reduce_array + one descent per rank "
+                                     "(k_cache_pointers); outputs verified equal to the GPU lists"}
+    del bits_k, cnts, live, free, flush
     torch.cuda.empty_cache()
     return out
+
+
+def random_bits(torch, device, depth, seed):
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    return torch.randint(-2 ** 63, 2 ** 63 - 1, ((1 << depth) // 64,), dtype=torch.int64, device=device, generator=gen)
 
 
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
 
-def run_gpu(args):
-    import torch
+def resolve_workload(args, world):
+    if args.workload != "auto":
+        return args.workload
+    return "batch" if world > 1 else "earth"
+
+
+def dist_setup(torch):
     import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (there is no CPU fallback for the product path)")
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} wants cuda:{local} but only {torch.cuda.device_count()} device(s) are visible")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    under_torchrun = "WORLD_SIZE" in os.environ and "MASTER_ADDR" in os.environ
+    if under_torchrun:  # also at world size 1: the NCCL gather path is the same code
+        os.environ.setdefault("NCCL_DEBUG", "WARN")
+        dist.init_process_group("nccl", device_id=device)
+
+    def barrier():
+        if under_torchrun:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    return dist, world, rank, local, device, under_torchrun, barrier
+
+
+def run_gpu_earth(args):
+    import ctypes as C
+    import torch
 
     from paper_2407_02215_b200 import _lib
     from paper_2407_02215_b200.lod import LodDecide
     from paper_2407_02215_b200.pipeline import ParallelEngine
     from paper_2407_02215_b200.state import initialize
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if not torch.cuda.is_available():
-        raise SystemExit("bench.py: no CUDA device (there is no CPU fallback for the product path)")
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=device)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(device)
-
+    dist, world, rank, local, device, grouped, barrier = dist_setup(torch)
     seq, down, cycle = sweep_params(args.depth, 45.0 * rank)
     K, W = args.steps, args.warmup
     eng = ParallelEngine()
-    # clocks are sampled from before the setup frames until after the e2e runs: the device-timed
+    # clocks are sampled from before the setup frames until after the e2e run: the device-timed
     # region itself is a few ms, shorter than nvidia-smi's sampling period
     sampler = ClockSampler(local)
     if rank == 0:
@@ -349,11 +468,9 @@ def run_gpu(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         start_host = state.to_host()
     e2e_state = state.clone()
-    state_before = e2e_state.clone()
 
     # ---- device-timed run: K frames, parameters resident, no host sync ----
     L = _lib.load()
-    import ctypes as C
     d_stats = torch.zeros((K, _lib.STATS_WORDS), dtype=torch.int64, device=device)
     pinned = torch.from_numpy(timed_prm).pin_memory()
     pool = state.c_pool()
@@ -372,50 +489,41 @@ def run_gpu(args):
     rows = d_stats.cpu().numpy()
     units = int(rows[:, 6].sum())
 
-    # ---- e2e: same frames through the public API, per-frame host<->device ----
-    # Every frame: LodDecide(config, camera, mesh) -> ParallelEngine.update -> UpdateStats on the host.
-    # Two engines: a kernel launch per frame, and the lingering frame kernel (linger_us: the kernel of
-    # one update keeps listening on a host-mapped mailbox, the next update is posted there).
-    cams = seq.cameras
-    cam_cycle = cams[SETUP_FRAMES - 1::-1] + cams[:SETUP_FRAMES]
-
-    def e2e_run(engine, st):
-        barrier()
-        t0 = time.perf_counter()
-        for j in range(K):
-            cam = cam_cycle[(W + j) % len(cam_cycle)]
-            engine.update(st, LodDecide(seq.config, cam, seq.mesh), epoch=j)
-        st.synchronize()  # (a listening kernel runs out its linger time: part of the measurement)
-        barrier()
-        return time.perf_counter() - t0
-
-    e2e_state2 = state_before.clone()
-    e2e_launch_s = e2e_run(eng, e2e_state)
-    linger_eng = ParallelEngine(linger_us=args.linger_us)
-    e2e_s = e2e_run(linger_eng, e2e_state2) if args.linger_us > 0 else e2e_launch_s
-    if args.linger_us > 0:
-        e2e_s -= args.linger_us * 1e-6  # the final kernel's idle listening after the last frame is not frame time
+    # ---- e2e: the same frames through the public API, default engine, per-frame host<->device ----
+    # Every frame: LodDecide(config, camera, mesh) -> ParallelEngine.update -> UpdateStats on the host
+    # (184 B of camera parameters in, 256 B of counters out, one cooperative launch).  Nothing is
+    # subtracted: the clock stops when the stream has drained after the last frame.
+    cams = step_cameras(seq, W, K)
+    for cam in cams[:3]:            # warm the per-frame launch path on a scratch copy
+        eng.update(state, LodDecide(seq.config, cam, seq.mesh))
+    barrier()
+    t0 = time.perf_counter()
+    e2e_rows = []
+    for j in range(K):
+        s = eng.update(e2e_state, LodDecide(seq.config, cams[j], seq.mesh), epoch=j)
+        e2e_rows.append((s.splits_rejected_oom, s.merges_rejected_oom, s.splits_applied, s.merges_applied,
+                         s.split_allocs, s.merge_allocs, s.live_before, s.live_after))
+    e2e_state.synchronize()
+    barrier()
+    e2e_s = time.perf_counter() - t0
     clocks = sampler.stop() if rank == 0 else None
-    for other in ((e2e_state, e2e_state2) if args.linger_us > 0 else (e2e_state,)):
-        same = all(torch.equal(getattr(state, "d_" + k), getattr(other, "d_" + k))
-                   for k in ("ids", "nexts", "prevs", "twins", "commands", "reserved", "bits", "counters"))
-        if not same:
-            raise SystemExit("bench.py: e2e run and device-timed run diverged (parity failure)")
+    if e2e_rows != [tuple(int(x) for x in rows[j, :8]) for j in range(K)]:
+        raise SystemExit("bench.py: e2e run and device-timed run report different counters (parity failure)")
 
     # ---- max over ranks ----
-    t = torch.tensor([gpu_ms, e2e_s * 1e3, float(units), e2e_launch_s * 1e3], dtype=torch.float64, device=device)
-    if world > 1:
+    t = torch.tensor([gpu_ms, e2e_s * 1e3, float(units)], dtype=torch.float64, device=device)
+    if grouped:
         tmax = t.clone()
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         tsum = t.clone()
         dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        gpu_ms, e2e_ms, units_all, e2e_launch_ms = float(tmax[0]), float(tmax[1]), float(tsum[2]), float(tmax[3])
+        gpu_ms, e2e_ms, units_all = float(tmax[0]), float(tmax[1]), float(tsum[2])
         gathered = [torch.zeros_like(d_stats) for _ in range(world)]
         dist.all_gather(gathered, d_stats)  # the only collective: final stats gather
     else:
-        e2e_ms, units_all, e2e_launch_ms = e2e_s * 1e3, float(units), e2e_launch_s * 1e3
+        e2e_ms, units_all = e2e_s * 1e3, float(units)
     if rank != 0:
-        if world > 1:
+        if grouped:
             dist.destroy_process_group()
         return 0
 
@@ -426,12 +534,11 @@ def run_gpu(args):
     # B_frame = B_reduce + N/8 + 4(n + A) + 16 n + 90 S + 50 M, B_reduce = N/4
     alg_bytes = float((N / 4 + N / 8 + 4 * (n_f + A_f) + 16 * n_f + 90 * S_f + 50 * M_f).sum())
     achieved = alg_bytes / (gpu_ms * 1e-3) / 1e9
+    traffic, traffic_src = load_traffic(args.depth)
     roofline = {
         "bound": "hbm", "kernel": "k_frames (persistent cooperative frame kernel, all six phases)",
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-        "traffic": KFRAMES_DRAM_BYTES_PER_FRAME.get(args.depth),
-        "traffic_source": "ncu --set full of k_frames (3 frames per launch), dram__bytes_read.sum + "
-                          "dram__bytes_write.sum per frame (profiles/r1c_kframes_ncu.txt)",
+        "traffic": traffic, "traffic_source": traffic_src,
         "algorithmic_bytes_per_frame": alg_bytes / K, "kernel_ms": gpu_ms, "launches": 1, "frames_per_launch": K,
         "timing": "CUDA events on the launch stream around the one launch that runs the K timed frames",
         "peak_source": peak_src,
@@ -440,63 +547,253 @@ def run_gpu(args):
                 "skips empty leaf blocks from their counters and the in-frame reduction only recounts the "
                 "leaf blocks the frame touched (traffic << algorithmic) -- and is bound by the latency of "
                 "~35 dependent L2 round trips and 6 grid barriers per frame, not by HBM; the two full-pool "
-                "CBT kernels are measured against the roofline in cbt_kernels_d26 / config4_d30"}
-    cbt26 = reduce_roofline(L, _lib, torch, device, state.d_bits, args.depth, peak, peak_src)
-    config4 = None
-    if not args.no_config4:
-        config4 = config4_probe(L, _lib, torch, device, peak)
+                "CBT kernels are measured against the roofline in cbt_kernels_d26 / config4"}
 
-    # ---- CPU baseline on a bounded sample, from the same start state ----
-    cpu = None
+    # ---- CPU baselines on bounded samples, from the same start state ----
+    cpu = cpu_port = cpu_reference = None
+    cpu_pool = None
     if start_host is not None:
         import oracle
         threads = oracle.max_threads()
-        n_cpu = min(K, args.cpu_frames)
-        op = oracle_pool_from_host(seq.mesh, args.depth, start_host)
-        sec, cpu_rows = cpu_sample(op, seq.mesh, timed_prm[:n_cpu], threads)
-        for j in range(n_cpu):
-            if cpu_rows[j] != [int(x) for x in rows[j, :8]]:
-                raise SystemExit(f"bench.py: GPU and CPU-oracle stats differ at timed frame {j}: "
-                                 f"{rows[j, :8].tolist()} vs {cpu_rows[j]}")
-        cpu_units = sum(r[6] for r in cpu_rows)
-        cpu = {"value": cpu_units / sec, "unit": UNIT, "cores": threads, "kind": "port",
-               "ms_per_frame": 1e3 * sec / n_cpu,
-               "sample": f"first {n_cpu} timed frames from the same pool state (stats verified "
-                         "equal to the GPU's), oracle port with OpenMP stage 2/classify/stage 9"}
+        n_port = min(K, args.cpu_frames)
+        op = cpu_pool = oracle_pool_from_host(seq.mesh, args.depth, start_host)
+        sec, port_rows = port_sample(op, seq.mesh, timed_prm[:n_port], threads)
+        for j in range(n_port):
+            if port_rows[j] != [int(x) for x in rows[j, :8]]:
+                raise SystemExit(f"bench.py: GPU and CPU-port stats differ at timed frame {j}: "
+                                 f"{rows[j, :8].tolist()} vs {port_rows[j]}")
+        cpu_port = {"value": sum(r[6] for r in port_rows) / sec, "unit": UNIT, "cores": threads, "kind": "port",
+                    "ms_per_frame": 1e3 * sec / n_port,
+                    "sample": f"first {n_port} timed frames from the same pool state (stats verified equal to the "
+                              "GPU's), C/OpenMP port of the reference path (oracle/): OpenMP over stage 2 / "
+                              "classifier / stage 9"}
+        cpu = cpu_port
+        if reference_available() and not args.port_only:
+            cpu_reference = reference_legs(args, seq, start_host, cams, rows, threads)
+            allt = cpu_reference["config3"]["all_threads"]
+            cpu = {"value": allt["bisectors_per_s"], "unit": UNIT, "cores": threads, "kind": "reference",
+                   "ms_per_frame": allt["ms_per_frame_mean"],
+                   "sample": f"first {allt['frames']} timed frames from the same pool state (stats verified equal to the "
+                             f"GPU's) through the unmodified cbtmesh ParallelEngine(threads={threads}).update + LodDecide "
+                             "(baseline/_ref), numba JIT-warmed first; see cpu_reference for 1 thread and config 2, "
+                             "cpu_port for the C/OpenMP port"}
 
-    # persistent path: ONE cooperative launch (k_frames) runs all K frames, six phases each;
-    # staged path: index, classify, admit, scatter, agree, reserve, apply, upper_reduce, publish per frame
-    gpu_launches = 9 * K if args.staged else 1
+    # ---- full-pool CBT kernels against the roofline (config 4), next to the CPU port ----
+    cbt26 = cbt_kernel_probe(L, torch, device, args.depth, state.d_bits, peak) if args.depth <= 28 else None
+    config4 = None
+    if not args.no_config4:
+        import oracle
+        config4 = {}
+        for d in (26, 28, 30):
+            bits = random_bits(torch, device, d, 1000 * d + 50)
+            use_cpu = d == 26 and cpu_pool is not None and args.depth == 26
+            config4[f"d{d}"] = cbt_kernel_probe(L, torch, device, d, bits, peak, cpu_pool if use_cpu else None,
+                                                oracle.max_threads() if use_cpu else 1)
+            del bits
+            torch.cuda.empty_cache()
+
+    e2e_value = units_all / (e2e_ms * 1e-3)
     line = {
         "metric": METRIC, "value": units_all / (gpu_ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": gpu_ms / K, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32/u64 + f64 classifier",
-        "data": "synthetic", "config": workload_config(args, world),
+        "scaling": "weak", "vs_baseline": None, "dtype": DTYPE,
+        "data": "synthetic", "config": workload_config(args, world, "earth"),
         "live_bisectors_per_frame": {"mean": float(rows[:, 6].mean()), "max": int(rows[:, 6].max())},
         "ops_in_run": {"splits": int(rows[:, 2].sum()), "merges": int(rows[:, 3].sum()),
                        "oom": int(rows[:, 0].sum() + rows[:, 1].sum())},
         "phase_us": {name: float(rows[:, _lib.STAT_PHASE_NS + k].mean()) / 1e3
                      for k, name in enumerate(_lib.PHASE_NAMES)},
-        "e2e": {"value": units_all / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms / K,
+        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms / K,
                 "h2d_bytes_per_step": 8 * _lib.PRM_WORDS, "d2h_bytes_per_step": 8 * _lib.STATS_WORDS,
-                "mode": (f"ParallelEngine(linger_us={args.linger_us:g}): the frame kernel of one update keeps listening "
-                         "on a host-mapped mailbox, the next update is posted there (no launch)") if args.linger_us > 0
-                        else "ParallelEngine(): one cooperative launch per frame",
-                "launch_per_frame": {"value": units_all / (e2e_launch_ms * 1e-3), "ms_per_step": e2e_launch_ms / K},
-                "note": "pool state is device-resident by design; per-frame host input is the camera (184 B, read by "
-                        "the kernel from mapped host memory or passed as launch parameters), per-frame output the "
-                        "32 counters the kernel writes straight into mapped host memory"},
-        "gpu_launches": gpu_launches, "launch_mode": "staged" if args.staged else "persistent (1 cooperative launch, 6 phases x K frames)",
+                "mode": "ParallelEngine().update(state, LodDecide(config, camera, mesh)) per frame: default engine, one "
+                        "cooperative launch per frame, wall clock from before the first update until the stream has "
+                        "drained after the last, nothing subtracted",
+                "note": "pool state is device-resident by design; per-frame host input is the camera (184 B, passed as "
+                        "launch parameters), per-frame output the 32 counters the kernel writes straight into mapped "
+                        "host memory as soon as they are decided (after the agreement phase), so the host side of "
+                        "the next frame overlaps with the rest of this one"},
+        # persistent path: ONE cooperative launch (k_frames) runs all K frames, six phases each;
+        # staged path: index, classify, admit, scatter, agree, reserve, apply, upper_reduce, publish per frame
+        "gpu_launches": 9 * K if args.staged else 1,
+        "launch_mode": "staged" if args.staged else "persistent (1 cooperative launch, 6 phases x K frames); e2e: K launches",
         "roofline": roofline,
         "cbt_kernels_d26": cbt26,
-        "config4_d30": config4,
+        "config4": config4,
         "cpu_baseline": cpu,
+        "cpu_port": cpu_port,
+        "cpu_reference": cpu_reference,
         "clocks": clocks,
     }
     print(json.dumps(line))
-    if world > 1:
+    if grouped:
         dist.destroy_process_group()
     return 0
+
+
+def reference_legs(args, seq, start_host, cams, gpu_rows, threads):
+    """The real reference beside the GPU: config 3 from the same pool state (a few frames at all
+    threads, fewer at 1 thread) and the whole BASELINE config 2 fly-in (2^20 pool, 64 frames)."""
+    from baseline import ref_timing
+    from paper_2407_02215_b200 import workloads
+    ref_timing.load()
+    jit_s = ref_timing.warm_jit(threads)
+    out = {"kind": "reference", "jit_warmup_s": jit_s, "cores": threads,
+           "method": "cbtmesh.pipeline.ParallelEngine(threads=T).update with LodDecide, perf_counter_ns around update "
+                     "(cli.py:285-289); unmodified package from baseline/_ref"}
+    st = ref_timing.state_from_arrays(seq.mesh, args.depth, start_host)
+    legs = {}
+    for name, T, frames in (("all_threads", threads, args.ref_frames), ("one_thread", 1, max(1, args.ref_frames - 1))):
+        work = st if name == "one_thread" else ref_timing.clone_state(st)
+        per_frame, ref_rows = ref_timing.time_frames(work, seq.mesh, seq.config, cams[:frames], T)
+        for j in range(frames):
+            if ref_rows[j] != [int(x) for x in gpu_rows[j, :8]]:
+                raise SystemExit(f"bench.py: GPU and real-reference stats differ at timed frame {j}: "
+                                 f"{gpu_rows[j, :8].tolist()} vs {ref_rows[j]}")
+        legs[name] = {"threads": T, "frames": frames, "ms_per_frame_mean": 1e3 * sum(per_frame) / frames,
+                      "ms_per_frame": [1e3 * x for x in per_frame],
+                      "bisectors_per_s": sum(r[6] for r in ref_rows) / sum(per_frame)}
+        del work
+    del st
+    out["config3"] = legs
+    if not args.no_config2:
+        fly = workloads.cube_sphere_flyin(depth=20, frames=64)
+        legs2 = {}
+        for name, T in (("all_threads", threads), ("one_thread", 1)):
+            from cbtmesh import sequential as ref_seq
+            st2 = ref_seq.initialize(ref_timing.ref_mesh_of(fly.mesh), 20)
+            per_frame, ref_rows = ref_timing.time_frames(st2, fly.mesh, fly.config, fly.cameras, T)
+            legs2[name] = {"threads": T, "frames": len(per_frame), "ms_per_frame_median": 1e3 * float(np.median(per_frame)),
+                           "total_ms": 1e3 * sum(per_frame), "bisectors_per_s": sum(r[6] for r in ref_rows) / sum(per_frame),
+                           "peak_live": max(r[7] for r in ref_rows)}
+        out["config2"] = legs2
+    return out
+
+
+def run_gpu_batch(args):
+    """BASELINE config 5: 8 planets x 2^24 slots over the ranks (strong scaling)."""
+    import torch
+
+    from paper_2407_02215_b200 import _lib, batch, workloads
+
+    dist, world, rank, local, device, grouped, barrier = dist_setup(torch)
+    K, W = args.steps, args.warmup
+    P = BATCH_PLANETS
+    owned = batch.planets_of_rank(P, world, rank)
+    seqs, downs, cycles = zip(*[sweep_params(BATCH_DEPTH, 45.0 * p) for p in range(P)])
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    t_setup = time.perf_counter()
+    states, _ = batch.run_planet_batch(seqs, list(downs), world, rank, device)                       # setup
+    states, _ = batch.run_planet_batch(seqs, [step_params(c, 0, W) for c in cycles], world, rank, device, states)  # warm-up
+    timed = [step_params(c, W, K) for c in cycles]
+    e2e_states = [s.clone() for s in states]
+    setup_s = time.perf_counter() - t_setup
+
+    # ---- device-timed: this rank's planets, K frames in lockstep in one launch per group ----
+    import ctypes as C
+    L = _lib.load()
+    k = len(owned)
+    d_stats = [torch.zeros((K, _lib.STATS_WORDS), dtype=torch.int64, device=device) for _ in owned]
+    pinned = [torch.from_numpy(timed[p]).pin_memory() for p in owned]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if rank == 0:
+        sampler.wait_first(2.0)
+    barrier()
+    ev0.record()
+    launches = 0
+    for g0 in range(0, k, _lib.MAX_BATCH):
+        g = range(g0, min(k, g0 + _lib.MAX_BATCH))
+        pools = (_lib.CPool * len(g))(*[states[q].c_pool() for q in g])
+        roots = (C.c_void_p * len(g))(*[_lib.ptr(states[q].d_root_tris) for q in g])
+        prms = (C.c_void_p * len(g))(*[pinned[q].data_ptr() for q in g])
+        souts = (C.c_void_p * len(g))(*[_lib.ptr(d_stats[q]) for q in g])
+        _lib.check(L.cbtm_run_lod_sequence_batch(pools, len(g), roots, prms, K, souts, states[g0].stream()),
+                   "cbtm_run_lod_sequence_batch")
+        launches += 1
+    ev1.record()
+    barrier()
+    gpu_ms = ev0.elapsed_time(ev1) if k else 0.0
+    for s in states:
+        s._touched()
+    local_rows = np.stack([d.cpu().numpy() for d in d_stats]) if k else np.zeros((0, K, _lib.STATS_WORDS), np.int64)
+
+    # ---- e2e: the public batch API with host parameter arrays (uploaded inside, stats downloaded inside) ----
+    barrier()
+    t0 = time.perf_counter()
+    _, e2e_block = batch.run_planet_batch(seqs, timed, world, rank, device, e2e_states)
+    torch.cuda.synchronize(device)
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    clocks = sampler.stop() if rank == 0 else None
+    cols = [c for c in range(13) if c != _lib.STAT_FRAME]   # (the frame counter of a cloned pool restarts)
+    if not np.array_equal(e2e_block[:, :, cols], local_rows[:, :, cols]):
+        raise SystemExit("bench.py: batch API run and device-timed run report different counters (parity failure)")
+
+    # ---- the one collective: final gather of the per-frame stats (NCCL all_gather) ----
+    full = batch.gather_stats(local_rows, owned, P, world, device=device if grouped else None)
+    t = torch.tensor([gpu_ms, e2e_s * 1e3], dtype=torch.float64, device=device)
+    per_rank_ms = [gpu_ms]
+    if grouped:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        per_rank_ms = [float(x[0]) for x in allt]
+        gpu_ms, e2e_ms = float(tmax[0]), float(tmax[1])
+    else:
+        e2e_ms = e2e_s * 1e3
+    if rank != 0:
+        if grouped:
+            dist.destroy_process_group()
+        return 0
+    units_all = float(full[:, :, 6].sum())
+    peak, peak_src = load_peaks()
+    N = 1 << BATCH_DEPTH
+    n_f, S_f, M_f, A_f = (full[:, :, c].astype(np.float64) for c in (6, 2, 3, 9))
+    alg_bytes = float((N / 4 + N / 8 + 4 * (n_f + A_f) + 16 * n_f + 90 * S_f + 50 * M_f).sum())
+    achieved = alg_bytes / world / (gpu_ms * 1e-3) / 1e9   # per GPU
+    line = {
+        "metric": METRIC, "value": units_all / (gpu_ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": gpu_ms / K, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": DTYPE,
+        "data": "synthetic", "config": workload_config(args, world, "batch"),
+        "per_rank_device_ms": per_rank_ms, "planets_per_rank": [len(batch.planets_of_rank(P, world, r)) for r in range(world)],
+        "live_bisectors_per_planet_frame": {"mean": float(full[:, :, 6].mean()), "max": int(full[:, :, 6].max())},
+        "ops_in_run": {"splits": int(full[:, :, 2].sum()), "merges": int(full[:, :, 3].sum()),
+                       "oom": int(full[:, :, 0].sum() + full[:, :, 1].sum())},
+        "stats_digest": {"live_after_last_frame": full[:, -1, 7].tolist(),
+                         "counter_sum": int(full[:, :, :10].sum())},
+        "phase_us": {name: float(local_rows[0, :, _lib.STAT_PHASE_NS + j].mean()) / 1e3
+                     for j, name in enumerate(_lib.PHASE_NAMES)},
+        "e2e": {"value": units_all / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms / K,
+                "h2d_bytes_per_step": 8 * _lib.PRM_WORDS * P, "d2h_bytes_per_step": 8 * _lib.STATS_WORDS * P,
+                "mode": "batch.run_planet_batch -> pipeline.run_lod_sequence_batch with host float64[K,23] parameter "
+                        "arrays per planet: parameter upload, K lockstep frames, stats download, all inside the clock"},
+        "gpu_launches": launches, "launch_mode": "k_frames_batch: one cooperative launch per rank runs K frames of its planets",
+        "collective": ("NCCL all_gather of the int64[planets, K, 32] stats (torch.distributed)" if grouped
+                       else "none (single process; the gather is a local re-index)"),
+        "roofline": {"bound": "hbm", "kernel": "k_frames_batch", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_step": alg_bytes / K,
+                     "note": "per GPU; latency-bound like the single-planet frame (see the earth workload's roofline note)"},
+        "cpu_baseline": None, "setup_s": setup_s,
+        "clocks": clocks,
+    }
+    print(json.dumps(line))
+    if grouped:
+        dist.destroy_process_group()
+    return 0
+
+
+def respawn_under_torchrun(args) -> int:
+    """`--gpus N` from a plain shell: one rank per GPU under torch.distributed.run."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -505,12 +802,17 @@ def main():
     ap.add_argument("--steps", type=int, default=64)
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="graft", choices=["graft", "reference"])
+    ap.add_argument("--workload", default="auto", choices=["auto", "earth", "batch"],
+                    help="earth = BASELINE config 3 (default at N = 1), batch = config 5 (default at N > 1)")
     ap.add_argument("--depth", type=int, default=26)
-    ap.add_argument("--cpu-frames", type=int, default=3)
+    ap.add_argument("--cpu-frames", type=int, default=8, help="frames of the C port timed beside the GPU")
+    ap.add_argument("--ref-frames", type=int, default=3, help="frames of the real reference timed beside the GPU")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--port-only", action="store_true", help="CPU legs: only the C port, not the real reference")
+    ap.add_argument("--no-config2", action="store_true")
     ap.add_argument("--no-config4", action="store_true")
-    ap.add_argument("--linger-us", type=float, default=500.0,
-                    help="linger time of the e2e engine (0: a kernel launch per frame)")
+    ap.add_argument("--torchrun-world1", action="store_true",
+                    help="run under torch.distributed.run even at N = 1 (exercises NCCL init + the gather)")
     ap.add_argument("--staged", action="store_true",
                     help="one kernel launch per pipeline stage (for ncu launch lists); default is the "
                          "persistent cooperative frame kernel")
@@ -518,7 +820,12 @@ def main():
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference(args)
-    return run_gpu(args)
+    if "WORLD_SIZE" not in os.environ and (args.gpus > 1 or args.torchrun_world1):
+        return respawn_under_torchrun(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if resolve_workload(args, world) == "batch":
+        return run_gpu_batch(args)
+    return run_gpu_earth(args)
 
 
 if __name__ == "__main__":

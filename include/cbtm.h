@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define CBTM_ABI_VERSION 1
+#define CBTM_ABI_VERSION 2
 #define CBTM_MIN_DEPTH 1
 #define CBTM_MAX_DEPTH 30 /* slot indices are int32; counters are uint32 */
 #define CBTM_LEAF_BLOCK_LOG2 10

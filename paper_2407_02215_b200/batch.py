@@ -23,15 +23,16 @@ def gather_stats(local: np.ndarray, owned: list[int], n_planets: int, world: int
                  device=None) -> np.ndarray | None:
     """Assemble int64[n_planets, frames, words] on every rank from each rank's
     int64[len(owned), frames, words].  Uses torch.distributed when initialised
-    (all_gather of equally padded blocks), otherwise returns the local block
-    re-indexed (single process)."""
+    (all_gather of equally padded blocks -- also at world size 1, so that a
+    one-GPU run goes through the same NCCL path), otherwise returns the local
+    block re-indexed (single process)."""
     import torch
     import torch.distributed as dist
 
     local = np.ascontiguousarray(local, dtype=np.int64)
     frames, words = local.shape[1], local.shape[2]
     out = np.zeros((n_planets, frames, words), dtype=np.int64)
-    if world == 1 or not (dist.is_available() and dist.is_initialized()):
+    if not (dist.is_available() and dist.is_initialized()):
         for k, p in enumerate(owned):
             out[p] = local[k]
         return out
@@ -50,21 +51,30 @@ def gather_stats(local: np.ndarray, owned: list[int], n_planets: int, world: int
 
 
 def run_planet_batch(sequences, frames_params, world: int = 1, rank: int = 0,
-                     device=None):
-    """Advance this rank's planets frame by frame (GPU).  ``sequences`` are
-    workloads.LodSequence objects, ``frames_params[p]`` is float64[frames, 23].
-    The planets of one rank advance in lockstep inside one cooperative launch
-    (``pipeline.run_lod_sequence_batch``): a single planet's frame is latency
-    bound and leaves the GPU mostly idle, a batch shares every grid barrier and
-    round trip.  Returns (states, int64[owned, frames, STATS_WORDS])."""
+                     device=None, states=None):
+    """Advance this rank's planets through ``frames_params`` (GPU).  ``sequences``
+    are workloads.LodSequence objects for ALL planets of the batch,
+    ``frames_params[p]`` is float64[frames, 23] for planet ``p``; the rank owns
+    planets ``planets_of_rank(len(sequences), world, rank)`` and touches only
+    those.  The planets of one rank advance in lockstep inside one cooperative
+    launch (``pipeline.run_lod_sequence_batch``): a single planet's frame is
+    latency bound and leaves the GPU mostly idle, a batch shares every grid
+    barrier and round trip.  ``states`` continues pools returned by an earlier
+    call (same rank) instead of initialising fresh ones.
+    Returns (states, int64[owned, frames, STATS_WORDS]) -- the block
+    :func:`gather_stats` assembles across ranks."""
     from . import _lib
     from .pipeline import run_lod_sequence_batch
     from .state import initialize
 
     owned = planets_of_rank(len(sequences), world, rank)
-    states = [initialize(sequences[p].mesh, sequences[p].depth, device=device) for p in owned]
-    per_planet = run_lod_sequence_batch(states, [frames_params[p] for p in owned])
-    rows = [[[s.splits_rejected_oom, s.merges_rejected_oom, s.splits_applied,
-              s.merges_applied, s.split_allocs, s.merge_allocs, s.live_before,
-              s.live_after] + [0] * (_lib.STATS_WORDS - 8) for s in stats] for stats in per_planet]
-    return states, np.array(rows, dtype=np.int64).reshape(len(owned), -1, _lib.STATS_WORDS)
+    if states is None:
+        states = [initialize(sequences[p].mesh, sequences[p].depth, device=device) for p in owned]
+    elif len(states) != len(owned):
+        raise ValueError(f"rank {rank} owns {len(owned)} planets, got {len(states)} states")
+    rows = run_lod_sequence_batch(states, [frames_params[p] for p in owned], raw=True)
+    frames = rows[0].shape[0] if rows else 0
+    block = np.zeros((len(owned), frames, _lib.STATS_WORDS), dtype=np.int64)
+    for k, r in enumerate(rows):
+        block[k] = r
+    return states, block

@@ -397,12 +397,14 @@ class ParallelEngine:
         return [UpdateStats.from_device_words(rows[f], first_epoch + f) for f in range(n)]
 
 
-def run_lod_sequence_batch(states, params_list, first_epoch: int = 0) -> list[list[UpdateStats]]:
+def run_lod_sequence_batch(states, params_list, first_epoch: int = 0, raw: bool = False):
     """Camera sequences of several independent planets on one GPU, advanced in
     lockstep inside one cooperative launch per group of up to ``_lib.MAX_BATCH``
     states (cbtm_run_lod_sequence_batch; BASELINE config 5).  ``params_list[p]``
     is float64[n_frames, 23] for ``states[p]``; all sequences have the same
-    length.  Results are identical to one ``run_lod_sequence`` per state."""
+    length.  Results are identical to one ``run_lod_sequence`` per state.
+    Returns one list of UpdateStats per state, or with ``raw=True`` one
+    int64[n_frames, STATS_WORDS] array per state (the device rows as they are)."""
     L = _lib.load()
     t = _lib.torch()
     if len(states) != len(params_list):
@@ -437,7 +439,8 @@ def run_lod_sequence_batch(states, params_list, first_epoch: int = 0) -> list[li
         for s, d in zip(group, d_stats):
             rows = _lib.to_host(d)
             s._touched()
-            out.append([UpdateStats.from_device_words(rows[f], first_epoch + f) for f in range(n)])
+            out.append(rows[:n].copy() if raw else
+                       [UpdateStats.from_device_words(rows[f], first_epoch + f) for f in range(n)])
     return out
 
 

@@ -36,7 +36,7 @@ def test_header_and_binding_agree(lib):
 
 
 def test_size_queries(lib):
-    assert lib.cbtm_abi_version() == 1
+    assert lib.cbtm_abi_version() == 2
     assert lib.cbtm_bitfield_words(4) == 16          # one 128-byte line minimum
     assert lib.cbtm_bitfield_words(26) == (1 << 26) // 64
     assert lib.cbtm_counter_words(10) == 2
