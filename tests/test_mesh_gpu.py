@@ -94,3 +94,17 @@ def test_device_built_mesh_drives_an_update():
     ha, hb = a.to_host(), b.to_host()
     for k in ha:
         assert np.array_equal(ha[k], hb[k]), k
+
+
+def test_device_ingest_rejects_malformed_csr_before_any_launch():
+    """Caller-supplied CSR offsets index device arrays directly: non-monotonic or mis-sized
+    offsets are rejected on the host with MeshError."""
+    import pytest
+    from paper_2407_02215_b200.halfedge import MeshError, from_polygons_device
+    pts = np.array([[0.0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0]])
+    verts = np.array([0, 1, 2, 0, 2, 3], dtype=np.int32)
+    good = from_polygons_device(pts, (np.array([0, 3, 6], dtype=np.int32), verts))
+    assert good.n_halfedges == 6
+    for offsets in ([0, 4, 3, 6], [1, 3, 6], [0, 3, 7], [0, 3, 5], [0]):
+        with pytest.raises(MeshError):
+            from_polygons_device(pts, (np.array(offsets, dtype=np.int32), verts))
