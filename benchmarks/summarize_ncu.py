@@ -21,7 +21,19 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
         "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "sm__cycles_active.avg",
-        "gpc__cycles_elapsed.max"]
+        "gpc__cycles_elapsed.max",
+        # atomic traffic (north_star: "atomic throughput against B200 peak")
+        "lts__t_sectors_op_atom.sum", "lts__t_sectors_op_red.sum", "lts__t_requests_op_atom.sum",
+        "lts__t_requests_op_red.sum", "lts__t_sectors_op_read.sum", "lts__t_sectors_op_write.sum",
+        "smsp__inst_executed_op_global_atom.sum", "smsp__inst_executed_op_global_red.sum",
+        "lts__t_sectors.avg.pct_of_peak_sustained_elapsed",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_fp64.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_alu.sum", "sm__inst_executed_pipe_lsu.sum",
+        "smsp__inst_executed.sum", "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct",
+        "smsp__warp_issue_stalled_barrier_per_warp_active.pct",
+        "smsp__warp_issue_stalled_membar_per_warp_active.pct"]
 
 
 def launches(path, first=None, last=None):
@@ -61,10 +73,10 @@ def details(path):
     seen = collections.OrderedDict()
     for r in rows[2:]:
         seen.setdefault(r[name_i].split("(")[0], []).append(r)
-    print(f"# ncu --set full summary of {path} (first launch of each kernel; {len(rows) - 2} launches captured)")
+    print(f"# ncu --set full summary of {path} (last captured launch of each kernel; {len(rows) - 2} launches captured)")
     for kname, rs in seen.items():
         print(f"\n## {kname}  ({len(rs)} launches)")
-        r = rs[0]
+        r = rs[-1]   # the last captured launch of the kernel (warm code, steady state)
         for k, i in idx.items():
             print(f"  {k:<62s} {r[i]:>16s} {units[i]}")
 
