@@ -288,6 +288,15 @@ int cbtm_sum_reduce(const uint64_t *bits, uint32_t *counters, int depth, void *w
 
 #ifdef CBTM_DEBUG_TIMING
 // debug builds only (benchmarks/reduce_probe.py): per-CTA stamps of the last k_sum_reduce launch
+extern "C" int cbtm_debug_probes(unsigned long long *host_out, int reset)
+{
+    int rc = status(cudaMemcpyFromSymbol(host_out, g_probe, sizeof(g_probe)));
+    if (rc == 0 && reset) {
+        static unsigned long long zeros[PROBE_FRAMES][PROBE_SLOTS];
+        rc = status(cudaMemcpyToSymbol(g_probe, zeros, sizeof(zeros)));
+    }
+    return rc;
+}
 extern "C" int cbtm_debug_reduce_stamps(unsigned long long *host_out, int n_ctas)
 {
     return status(cudaMemcpyFromSymbol(host_out, g_reduce_stamps, sizeof(unsigned long long) * 5 * n_ctas));

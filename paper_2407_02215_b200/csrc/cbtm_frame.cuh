@@ -59,8 +59,35 @@
 // relative to the phase start, in ns), to tell work from barrier wait (benchmarks/phase_probe.py)
 #ifdef CBTM_DEBUG_TIMING
 #define WORK_END(ctl, k) do { if (threadIdx.x == 0) atomicMax(&(ctl)->work_end[k], global_ns()); } while (0)
+// finer probes (benchmarks/probe_phases.py): latest arrival of any CTA at a point of the frame, per
+// frame of a sequence run; slots 0..6 = phase starts as stamped by CTA 0
+#define PROBE_FRAMES 128
+#define PROBE_SLOTS 32
+#define PROBE(slot)                                                                                      \
+    do {                                                                                                 \
+        __syncthreads();                                                                                 \
+        if (threadIdx.x == 0) atomicMax(&cbtm::g_probe[cbtm::probe_frame() & (PROBE_FRAMES - 1)][slot], cbtm::probe_now()); \
+    } while (0)
+#define PROBE_SET_FRAME(f) do { if (threadIdx.x == 0) cbtm::probe_frame() = (f); __syncthreads(); } while (0)
+#define PROBE_T0(slot, f)                                                                                \
+    do {                                                                                                 \
+        if (blockIdx.x == 0 && threadIdx.x == 0) cbtm::g_probe[(f) & (PROBE_FRAMES - 1)][slot] = cbtm::probe_now(); \
+    } while (0)
+namespace cbtm {
+__device__ unsigned long long g_probe[PROBE_FRAMES][PROBE_SLOTS];
+__device__ __forceinline__ int &probe_frame() { __shared__ int f; return f; }
+__device__ __forceinline__ unsigned long long probe_now()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+} // namespace cbtm
 #else
 #define WORK_END(ctl, k) do { } while (0)
+#define PROBE(slot) do { } while (0)
+#define PROBE_SET_FRAME(f) do { } while (0)
+#define PROBE_T0(slot, f) do { } while (0)
 #endif
 
 #include "cbtm_cbt.cuh"
@@ -462,6 +489,7 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
             }
             gathered = {id, js, jo, sib, oth, j4, nx, pv};
         }
+        PROBE(8); // classify: gathers issued (loads may still be in flight)
         { // deepest live bisector of the frame
             const int d = i < n ? depth_of(gathered.id, p.rank) : 0;
             acc_depth = max(acc_depth, __reduce_max_sync(FULL_MASK, d));
@@ -496,8 +524,8 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
             a.ws.need8[i] = (uint8_t)need;
             a.ws.mbits8[i] = (uint8_t)mbits;
         }
+        PROBE(9); // classify: verdicts and needs known
 #ifdef CBTM_DEBUG_TIMING
-        __syncthreads();
         WORK_END(ctl, 0);
 #endif
         uint32_t sum = warp_sum(need);
@@ -507,6 +535,7 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
                 atomicOr(&p.commands[s], mbits);
             else if (need)
                 walk_split_chain(p, s);
+            PROBE(10); // classify: commands scattered
             continue;
         }
         uint32_t mn = need ? need : 255u;
@@ -916,6 +945,7 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, ui
         off += (long long)cta_range_sum(a.ws.chunk_alloc, summed, chunk, scratch64);
         summed = chunk;
         if (total == 0) continue; // CTA-uniform
+        PROBE(14); // reserve: prefix known
         uint32_t total_chk;
         const uint32_t incl = block_inclusive_scan<CHUNK>(na, scratch, &total_chk);
 
@@ -938,6 +968,7 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, ui
                 top -= CHUNK;
             }
             WORK_END(ctl, 7); // window block found
+            PROBE(15);
             // The interval may span many leaf blocks when the pool is dense around it (few free slots per
             // block): a warp per block, and the next block's table entry and bits are fetched while the
             // current one is expanded (one round trip per block otherwise).
@@ -977,6 +1008,7 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, ui
             }
             __syncthreads();
             WORK_END(ctl, 8); // slots expanded
+            PROBE(16);
         }
         if (na) {
             for (uint32_t k = 0; k < na; ++k) {
@@ -1471,13 +1503,17 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
     for (int f = 0; f < n_frames || mailbox; ++f) {
         unsigned long long *stamp = stamper ? ctl->phase_t[f & 1] : nullptr;
         if (stamp) stamp[0] = global_ns();
+        PROBE_SET_FRAME(f);
+        PROBE_T0(0, f);
         if (do_index)
             index_phase<true>(reinterpret_cast<const uint32_t *>(p.bits), p.counters, p.depth, p.cache_live,
                         free_list, p.dispatch, p.commands,
                         reinterpret_cast<int32_t(*)[IDX_STAGE_WORDS]>(dyn_smem), bid, nb);
         else
             phase_reset(a, bid, nb);
+        PROBE(7); // index work done
         grid.sync();
+        PROBE_T0(1, f);
         if (stamp) stamp[1] = global_ns();
         const uint32_t n = p.counters[1];      // the frame's live count: one read per CTA, kept in a register
         const bool fast = fits_a_priori(p, n); // grid-uniform
@@ -1496,16 +1532,20 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
             grid.sync();
         }
         if (stamp) stamp[2] = global_ns();
+        PROBE_T0(2, f);
         // T is final: the free-rank window table is built by the CTA with the fewest chunks while the
         // others take the agreement snapshot (it was the straggler of P2 when built there)
         if (bid == nb - 1) {
             frame_totals(a, n, fits);
             build_window_table(a, ctl->T);
+            PROBE(12); // window table built
         }
         phase_agree(a, n, bid, nb);
+        PROBE(13); // agreement done
         WORK_END(ctl, 2);
         grid.sync();
         if (stamp) stamp[3] = global_ns();
+        PROBE_T0(3, f);
         // The launch's last frame: every counter of the frame is decided (admission, agreement,
         // allocation counts), so they go to the host NOW, three phases before the frame is done --
         // ParallelEngine.update returns on them and the host's work between two frames (stats
@@ -1515,19 +1555,25 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         if (bid == nb - 1 && !mailbox && f == n_frames - 1 && p.stats)
             publish_early(ctl->stats, p.stats, ctl->phase_t[f & 1], threadIdx.x);
         phase_reserve(a, n, bid, nb);
+        PROBE(17); // reserve done
         WORK_END(ctl, 3);
         grid.sync();
         if (stamp) stamp[4] = global_ns();
+        PROBE_T0(4, f);
         phase_apply(a, n, bid, nb);
+        PROBE(20); // apply done
         WORK_END(ctl, 4);
         grid.sync();
+        PROBE_T0(5, f);
         if (stamp) {
             stamp[5] = global_ns();
             __threadfence(); // read by the publishing CTA after the next barrier
         }
         upper_reduce_phase(p.bits, a.ws.dirty, p.counters, g.lc, reinterpret_cast<uint32_t *>(dyn_smem), wroot, bid, nb);
+        PROBE(22); // reduce done
         WORK_END(ctl, 5);
         grid.sync();
+        PROBE_T0(6, f);
         // the frame's counters go out while the next frame's index phase is already running
         // (pool->stats may be host-mapped memory: only the launch's last frame pays for that write)
         if (bid == nb - 1) {
