@@ -259,6 +259,17 @@ class ParallelEngine:
         # the reference reads cbt.count() first, which asserts a reduced tree (pipeline.py:211, cbt.py:70-73)
         assert not state.cbt._dirty, "sum_reduce required before count()"
         cv = decide.device_verdict(state) if isinstance(decide, KernelDecide) else None
+        if cv is not None and self.profile:
+            # device verdict source, profiled: wait for the COMPLETE row (written when the frame has been
+            # reduced) -- the six device phase timers fold onto the reference's nine stage slots
+            seq_before = int(state._stats_np[_lib.STAT_SEQ])
+            _lib.check(L.cbtm_update(state.c_pool_ref(), cv, state.stream()), "cbtm_update")
+            rc = L.cbtm_wait_frame_done(state._stats_host_ptr, seq_before + 1, 20_000_000_000)
+            if rc:
+                state.synchronize()
+                _lib.check(rc, "cbtm_wait_frame_done")
+            state._touched()
+            return _checked(UpdateStats.from_device_words(state._stats_np.tolist(), epoch))
         if cv is not None and not self.profile and not (self.linger_ns and cv.mode == _lib.VERDICT_LOD):
             # device verdict source: stages 1-9 in one cooperative launch; launch + wait for the
             # frame's counters in ONE call into the library

@@ -264,3 +264,27 @@ def test_peak_depth_is_reduced_on_the_device():
         assert rows[0].peak_depth == before
         after = max(bisector.depth_of(int(b), st.rank) for b in st.ids[st.live_slots()])
         assert eng.update(st, KeepAll()).peak_depth == after
+
+
+def test_profile_engine_reports_all_device_phase_times():
+    """ParallelEngine(profile=True) waits for the frame's complete row: the six device phase timers
+    folded onto the reference's nine `stage_times_us` slots (pipeline.py:218-223), same counters as the
+    default engine, which returns on the early row (phases 4-6 not timed yet, no poison count)."""
+    from paper_2407_02215_b200 import workloads
+    seq = workloads.cube_sphere_flyin(depth=16, frames=10)
+    a = initialize(seq.mesh, 16)
+    b = initialize(seq.mesh, 16)
+    fast, prof = ParallelEngine(), ParallelEngine(profile=True)
+    for i, cam in enumerate(seq.cameras):
+        sa = fast.update(a, lod.LodDecide(seq.config, cam, seq.mesh), epoch=i)
+        sb = prof.update(b, lod.LodDecide(seq.config, cam, seq.mesh), epoch=i)
+        assert sa.csv_row(no_timing=True) == sb.csv_row(no_timing=True)
+        assert all(t > 0 for t in sb.phase_ns), sb.phase_ns
+        t = sb.stage_times_us
+        assert len(t) == 9 and t[1] > 0 and t[3] > 0 and t[4] > 0 and t[5] > 0 and t[8] > 0
+        assert sa.phase_ns[0] > 0 and sa.phase_ns[1] > 0 and sa.phase_ns[2] > 0
+        assert sa.phase_ns[3:] == [0, 0, 0] or sa.phase_ns[5] > 0      # early row (or the complete one if it won the race)
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(a.to_host()["nodes"], b.to_host()["nodes"])
+    # python-callable verdicts under profiling: the begin / finish spans are timed with events
+    s = prof.update(b, lambda bid: 0, epoch=99)
+    assert s.structural_ops == 0 and s.stage_times_us[1] > 0 and s.stage_times_us[3] > 0

@@ -191,3 +191,101 @@ def test_held_view_of_a_pool_cbt_survives_an_engine_update():
     st.cbt.sum_reduce()
     assert st.cbt.count() == live + 1 and st.cbt.get_bit(free) == 1
     assert int(lv.sum()) == live + 1   # the view shows the device's leaves plus the write
+
+
+# -- the two ways k_sum_reduce builds the levels above the tile roots ----------------
+
+def _heap_on_device(bits, counters, depth):
+    import torch
+    from paper_2407_02215_b200 import _lib
+    nodes = torch.empty(2 << depth, dtype=torch.int32, device=bits.device)
+    _lib.check(_lib.load().cbtm_export_nodes(_lib.ptr(bits), _lib.ptr(counters), depth, _lib.ptr(nodes),
+                                             _lib.stream_handle(bits.device)), "cbtm_export_nodes")
+    return nodes
+
+
+def _consistent(nodes, depth):
+    """every internal node == sum of its children, on the device"""
+    n = 1 << depth
+    inner = nodes[1:n].to(int)
+    kids = nodes[2:2 * n].to(int).view(-1, 2).sum(dim=1)
+    return bool((inner == kids).all())
+
+
+@pytest.mark.parametrize("depth", [10, 17, 18, 19, 21, 24, 26, 28])
+def test_sum_reduce_rebuild_and_delta_paths_agree_with_the_oracle(depth):
+    """k_sum_reduce: an unstamped tree (fresh, zeroed or garbage counters) is rebuilt by the last CTA
+    and stamped; a stamped tree takes per-tile atomic deltas -- after arbitrary changes of the
+    bitfield, repeatedly, with statically dealt and (2^28) dynamically claimed tiles.  Every level
+    against the oracle's heap up to 2^24, against the sum-of-children property and the popcount above."""
+    import torch
+    from paper_2407_02215_b200 import _lib
+    L = _lib.load()
+    dev = torch.device("cuda", 0)
+    n = 1 << depth
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(4242 + depth)
+    words = max(16, n // 64)
+    lut = torch.tensor([bin(i).count("1") for i in range(256)], dtype=torch.int64, device=dev)
+
+    def popcount(b):
+        return int(sum(int(lut[b[lo:lo + (1 << 22)].view(torch.uint8).to(torch.int64)].sum())
+                       for lo in range(0, b.numel(), 1 << 22)))
+
+    def random_bits(density_and):
+        b = torch.randint(-2 ** 63, 2 ** 63 - 1, (words,), dtype=torch.int64, device=dev, generator=gen)
+        for _ in range(density_and):
+            b &= torch.randint(-2 ** 63, 2 ** 63 - 1, (words,), dtype=torch.int64, device=dev, generator=gen)
+        if n < 64 * words:       # tiny pools: only the low n bits exist
+            b[n // 64:] = 0
+        return b
+
+    ws = torch.zeros(1024, dtype=torch.uint8, device=dev)
+    stream = _lib.stream_handle(dev)
+    bits = random_bits(0)
+    counters = torch.randint(0, 2 ** 31 - 1, (L.cbtm_counter_words(depth),), dtype=torch.int32, device=dev, generator=gen)
+    counters[0] = 12345                     # garbage everywhere, no stamp
+
+    def reduce_and_check(tag):
+        _lib.check(L.cbtm_sum_reduce(_lib.ptr(bits), _lib.ptr(counters), depth, _lib.ptr(ws), 1024, stream), tag)
+        nodes = _heap_on_device(bits, counters, depth)
+        assert int(nodes[1]) == popcount(bits), tag
+        assert _consistent(nodes, depth), tag
+        assert int(ws.view(torch.int32)[0]) == 0 and int(ws.view(torch.int32)[1]) == 0, tag   # ticket + claim counter
+        if depth <= 24:
+            import oracle
+            host = np.zeros(2 * n, np.uint32)
+            host[n:] = np.unpackbits(bits.cpu().numpy().view(np.uint8), bitorder="little")[:n]
+            oracle.sum_reduce_nodes(host, depth, threads=8)
+            assert np.array_equal(nodes.cpu().numpy().view(np.uint32), host), tag
+        return nodes
+
+    reduce_and_check("rebuild from garbage counters")
+    stamp = int(counters[0])
+    assert stamp != 12345 and stamp != 0
+    for round_, density in enumerate((0, 3, 1, 0)):
+        bits.copy_(random_bits(density))                      # a completely different bitfield
+        if round_ == 2:
+            bits[:bits.numel() // 3] = 0                      # a long empty prefix
+        reduce_and_check(f"delta round {round_}")
+        assert int(counters[0]) == stamp
+    bits[::5] ^= 0x0F0F                                       # sparse changes
+    reduce_and_check("delta after sparse flips")
+    counters.zero_()                                          # a caller reset the counters: rebuild again
+    reduce_and_check("rebuild from zeroed counters")
+    assert int(counters[0]) == stamp
+
+
+def test_sum_reduce_rejects_misaligned_counters():
+    import torch
+    from paper_2407_02215_b200 import _lib
+    L = _lib.load()
+    dev = torch.device("cuda", 0)
+    bits = torch.zeros(1 << 10, dtype=torch.int64, device=dev)
+    counters = torch.zeros(L.cbtm_counter_words(16) + 4, dtype=torch.int32, device=dev)
+    ws = torch.zeros(1024, dtype=torch.uint8, device=dev)
+    out = torch.zeros(8, dtype=torch.int32, device=dev)
+    bad = counters.data_ptr() + 4
+    assert L.cbtm_sum_reduce(bits.data_ptr(), bad, 16, ws.data_ptr(), 1024, 0) == 6           # CBTM_E_ALIGN
+    assert L.cbtm_decode_ones(bits.data_ptr(), bad, 16, None, 8, out.data_ptr(), 0) == 6
+    assert L.cbtm_index(bits.data_ptr(), bad, 16, out.data_ptr(), None, None, 0) == 6
