@@ -13,16 +13,20 @@ from paper_2407_02215_b200.pipeline import ParallelEngine, lod_verdict
 from paper_2407_02215_b200.state import initialize
 
 depth = int(sys.argv[1]) if len(sys.argv) > 1 else 26
+first = int(sys.argv[2]) if len(sys.argv) > 2 else 0     # bench.py times frames [warmup, warmup + K) of the cycle
 seq, down, cycle = bench.sweep_params(depth, 0.0)
 eng = ParallelEngine()
 state = initialize(seq.mesh, depth)
 eng.run_lod_sequence(state, down)
+if first:
+    eng.run_lod_sequence(state, bench.step_params(cycle, 0, first))
 start = state.clone()
 cams = seq.cameras
 cam_cycle = cams[bench.SETUP_FRAMES - 1::-1] + cams[:bench.SETUP_FRAMES]
 L = _lib.load()
 K = 64
 pc = time.perf_counter
+cam_cycle = [cam_cycle[(first + j) % len(cam_cycle)] for j in range(K)]
 decs = [LodDecide(seq.config, cam_cycle[j], seq.mesh) for j in range(K)]   # kept alive: their buffers are read below
 prm = np.stack([d._prm for d in decs])
 cvs = []

@@ -74,6 +74,12 @@ extern "C" {
 #define CBTM_POOL_WIDE_GRID 8u /* persistent frame kernel with 4 instead of 2 CTAs per SM: pays off from
                                  ~10^5 live bisectors on (each CTA then works through several chunks of
                                  256 ranks per phase); same results */
+#define CBTM_POOL_FINAL_ROW 16u /* cbtm_update also writes the frame's COMPLETE stats row (poison count of this
+                                  frame, times of all six phases) and CBTM_STAT_DONE to pool->stats when the
+                                  frame has been reduced.  Default for a single-frame launch: only the early
+                                  row (see CBTM_STAT_SEQ) -- the kernel then ends with its reduction, without a
+                                  device-wide barrier and a host write behind it; a poison count (an error
+                                  condition, 0 by construction) is carried over into the next frame's row */
 #define CBTM_POOL_STAGED_LAUNCHES 2u /* one kernel launch per pipeline stage instead of
                                         the persistent cooperative frame kernel (per-stage
                                         profiling; automatic where cooperative launch is
@@ -104,11 +110,12 @@ enum {
                               * and allocation counts decide all of them; live_after = live_before -
                               * freed + allocated), while stages 5b-9 are still running on the stream --
                               * the host-side work between two frames overlaps with them and the next
-                              * launch is queued behind a running kernel.  Not in that early copy: the
-                              * poison count (0) and the times of phases 4-6 (words 19-21); the complete
-                              * row follows at the end of the frame: */
+                              * launch is queued behind a running kernel.  Not in that early copy: this
+                              * frame's poison count and the times of phases 4-6 (words 19-21); with
+                              * CBTM_POOL_FINAL_ROW (and in multi-frame launches) the complete row follows
+                              * at the end of the frame: */
     CBTM_STAT_DONE = 30,     /* = CBTM_STAT_FRAME, stored after the frame's reduction and the complete
-                              * row (cbtm_wait_frame_done) */
+                              * row (cbtm_wait_frame_done; single-frame launches: needs CBTM_POOL_FINAL_ROW) */
     /* words 16..21: device time of each phase of the frame in ns (persistent
      * frame kernel only; 0 on the staged path): index (stages 1-3), classify +
      * admission + command scatter (stage 4), merge agreement (stage 5a), slot

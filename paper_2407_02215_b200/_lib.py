@@ -31,6 +31,7 @@ POOL_FULL_FREE_CACHE = 1
 POOL_STAGED_LAUNCHES = 2
 POOL_DESCEND_FREE_RANKS = 4
 POOL_WIDE_GRID = 8
+POOL_FINAL_ROW = 16
 
 VERDICT_CONST, VERDICT_UNIFORM, VERDICT_LOD, VERDICT_EXPLICIT = 0, 1, 2, 3
 

@@ -108,7 +108,7 @@ __device__ __forceinline__ void publish_early(const int64_t *ctl_stats, int64_t 
     }
     if (tid == CBTM_STAT_LIVE_AFTER) v = live_after;
     if (tid == CBTM_STAT_ALLOCATED) v = allocated;
-    if (tid == CBTM_STAT_POISON) v = 0;
+    // (word CBTM_STAT_POISON: whatever earlier frames left unreported -- see retire_frame)
     if (tid == CBTM_STAT_FRAME) v += 1;
     const int64_t frame = __shfl_sync(FULL_MASK, v, CBTM_STAT_FRAME);
     if (tid >= CBTM_STAT_PHASE_NS && tid < CBTM_STAT_PHASE_NS + CBTM_STAT_PHASES) {
@@ -124,6 +124,20 @@ __device__ __forceinline__ void publish_early(const int64_t *ctl_stats, int64_t 
     __threadfence_system();
     __syncwarp();
     if (tid == CBTM_STAT_SEQ) *(volatile int64_t *)&pool_stats[tid] = frame;
+}
+
+// End-of-frame bookkeeping of a single-frame launch that publishes only the early row: frame
+// counter, per-frame counters back to zero.  Runs right behind the barrier that ends the apply
+// phase (every counter is final then), next to the reduction, so that the kernel can end with
+// its reduction work -- no device-wide barrier and no host write on its tail.  The poison count
+// is NOT reset: nobody has reported it yet, the next frame's row will.  One warp.
+__device__ __forceinline__ void retire_frame(int64_t *ctl_stats, uint32_t *seq_frame, int tid)
+{
+    if (tid < CBTM_STAT_PHASE_NS) {
+        if (tid == CBTM_STAT_FRAME) ctl_stats[tid] += 1;
+        else if (tid != CBTM_STAT_POISON) ctl_stats[tid] = 0;
+    }
+    if (tid == 0) *seq_frame += 1;
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)

@@ -1569,9 +1569,14 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
             stamp[5] = global_ns();
             __threadfence(); // read by the publishing CTA after the next barrier
         }
+        // cbtm_update (one frame, counters already on the host since P3): the frame is retired here and
+        // the kernel ends with its reduction work, without a barrier and a host write on its tail
+        const bool early_only = n_frames == 1 && !mailbox && !stats_seq && p.stats && !(p.flags & CBTM_POOL_FINAL_ROW);
+        if (early_only && bid == nb - 1 && threadIdx.x < 32) retire_frame(ctl->stats, &ctl->seq_frame, threadIdx.x);
         upper_reduce_phase(p.bits, a.ws.dirty, p.counters, g.lc, reinterpret_cast<uint32_t *>(dyn_smem), wroot, bid, nb);
         PROBE(22); // reduce done
         WORK_END(ctl, 5);
+        if (early_only) break; // grid-uniform
         grid.sync();
         PROBE_T0(6, f);
         // the frame's counters go out while the next frame's index phase is already running
@@ -1637,7 +1642,10 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
 // of one.  Pool q sees the CTAs rotated by q * nb / P, which spreads the chunks
 // (and the admin / single-CTA duties) of the pools over different SMs.
 // ---------------------------------------------------------------------------
-constexpr int BATCH_CTAS_PER_SM = 4; // more chunks in flight per SM: a batch has work for them
+#ifndef CBTM_BATCH_CTAS_PER_SM
+#define CBTM_BATCH_CTAS_PER_SM 4
+#endif
+constexpr int BATCH_CTAS_PER_SM = CBTM_BATCH_CTAS_PER_SM; // more chunks in flight per SM: a batch has work for them
 
 struct BatchArgs {
     FrameArgs a[CBTM_MAX_BATCH];

@@ -48,7 +48,8 @@ class UpdateStats:
     merge_allocs: int
     stage_times_us: list = field(default_factory=lambda: [0] * 9)
     reserved_slots: int = 0   # T: slots reserved by admitted commands
-    poison: int = 0           # fresh pointers that resolved to the poison -2
+    poison: int = 0           # fresh pointers that resolved to the poison -2 (0 by construction; update() reports
+                              # what EARLIER frames found: its row leaves the device before stage 6 runs)
     phase_ns: list = field(default_factory=lambda: [0] * 6)  # device ns per phase (_lib.PHASE_NAMES)
     peak_depth: int = 0       # deepest live bisector at the start of the frame (cli.py:232-237, on device)
 
@@ -262,6 +263,7 @@ class ParallelEngine:
         if cv is not None and self.profile:
             # device verdict source, profiled: wait for the COMPLETE row (written when the frame has been
             # reduced) -- the six device phase timers fold onto the reference's nine stage slots
+            state.complete_rows = True      # CBTM_POOL_FINAL_ROW
             seq_before = int(state._stats_np[_lib.STAT_SEQ])
             _lib.check(L.cbtm_update(state.c_pool_ref(), cv, state.stream()), "cbtm_update")
             rc = L.cbtm_wait_frame_done(state._stats_host_ptr, seq_before + 1, 20_000_000_000)
@@ -281,6 +283,8 @@ class ParallelEngine:
                 _lib.check(rc, "cbtm_update_wait")
             state._touched()
             return _checked(UpdateStats.from_device_words(state._stats_np.tolist(), epoch))
+        if self.profile:
+            state.complete_rows = True
         pool = state.c_pool()
         stream = state.stream()
         seq_before = int(state._stats_np[_lib.STAT_SEQ])

@@ -72,6 +72,9 @@ class TriangulationState:
         # testing hook: free ranks by tree descent instead of the window table (the fallback for
         # frames whose allocations span more than 4096 leaf blocks)
         self.descend_free_ranks = bool(descend_free_ranks)
+        # cbtm_update also writes the frame's complete stats row at the end of the frame
+        # (CBTM_POOL_FINAL_ROW; set by ParallelEngine(profile=True))
+        self.complete_rows = False
         self.device = _lib.require_cuda(device)
         L = _lib.load()
         t = _lib.torch()
@@ -129,7 +132,8 @@ class TriangulationState:
         # wide grid (4 CTAs per SM) once the pool holds more live bisectors than the narrow grid has
         # threads for two chunks each; decided from the last published live count (host-mapped stats)
         wide = int(self._stats_np[7]) > WIDE_GRID_LIVE
-        key = (int(self.max_depth), self.exact_free_cache, self.staged_launches, self.descend_free_ranks, wide)
+        key = (int(self.max_depth), self.exact_free_cache, self.staged_launches, self.descend_free_ranks, wide,
+               self.complete_rows)
         cached = getattr(self, "_c_pool", None)
         if cached is not None and cached[0] == key:
             return cached[1]
@@ -158,7 +162,8 @@ class TriangulationState:
             (_lib.POOL_FULL_FREE_CACHE if self.exact_free_cache else 0)
             | (_lib.POOL_STAGED_LAUNCHES if self.staged_launches else 0)
             | (_lib.POOL_DESCEND_FREE_RANKS if self.descend_free_ranks else 0)
-            | (_lib.POOL_WIDE_GRID if wide else 0))
+            | (_lib.POOL_WIDE_GRID if wide else 0)
+            | (_lib.POOL_FINAL_ROW if self.complete_rows else 0))
 
     def _touched(self) -> None:
         """The device arrays changed: drop host snapshots."""
