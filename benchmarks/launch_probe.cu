@@ -110,7 +110,29 @@ int main()
                kernel_us / K, per - kernel_us / K, call_us / K);
         return 0;
     };
-    for (int rep = 0; rep < 2; ++rep) {
+    // the same launch call while the previous kernel is still running (queued, no host wait)
+    for (int coop = 0; coop < 2; ++coop) {
+        a.coop = coop;
+        a.spin_ns = 36000;
+        CK(cudaStreamSynchronize(st));
+        double call_us = 0;
+        const int Q = 64;
+        for (int i = 0; i < Q; ++i) {
+            a.seq = 1;
+            auto c0 = std::chrono::steady_clock::now();
+            if (coop) {
+                void *args[] = {&a, (void *)&ring, (void *)&out};
+                CK(cudaLaunchCooperativeKernel((const void *)k_frame, dim3(grid), dim3(256), args, 0, st));
+            } else {
+                k_frame<<<grid, 256, 0, st>>>(a, ring, out);
+            }
+            call_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - c0).count();
+        }
+        CK(cudaStreamSynchronize(st));
+        printf("%-44s launch call %4.1f us while the previous kernel runs (%d queued)\n",
+               coop ? "cudaLaunchCooperativeKernel, queued" : "plain <<<>>>, queued", call_us / Q, Q);
+    }
+    for (int rep = 0; rep < 1; ++rep) {
         if (run("cudaLaunchCooperativeKernel", 0)) return 1;
         if (run("plain <<<>>> (no grid barriers)", 1)) return 1;
         if (run("cudaLaunchKernelEx + cooperative attribute", 2)) return 1;

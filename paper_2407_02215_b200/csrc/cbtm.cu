@@ -244,6 +244,10 @@ unsigned persistent_grid(int depth, bool wide = false)
 
 inline bool wide(const cbtm_pool *pool) { return (pool->flags & CBTM_POOL_WIDE_GRID) != 0; }
 
+#ifdef CBTM_DEBUG_TIMING
+long long g_launch_ns = 0, g_launch_calls = 0;
+#endif
+
 // n_frames full updates (optionally without the index phase) in one cooperative launch; with a
 // mailbox: one update, then the kernel lingers for further requests (cbtm_update_linger)
 int frames_launch(FrameArgs &a, int n_frames, int64_t *stats_seq, int do_index, unsigned grid, cudaStream_t st,
@@ -252,7 +256,27 @@ int frames_launch(FrameArgs &a, int n_frames, int64_t *stats_seq, int do_index, 
     void *args[] = {(void *)&a,       (void *)&n_frames,  (void *)&stats_seq,   (void *)&do_index,
                     (void *)&mailbox, (void *)&linger_ns, (void *)&next_request};
     const void *kernel = wide(&a.pool) ? (const void *)k_frames<4> : (const void *)k_frames<2>;
-    return status(cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(CHUNK), args, FRAMES_DYN_SMEM, st));
+    // (cudaLaunchKernelExC with the cooperative attribute: ~1 us less host time per call than
+    //  cudaLaunchCooperativeKernel, benchmarks/launch_probe.cu)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(CHUNK);
+    cfg.dynamicSmemBytes = FRAMES_DYN_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+#ifdef CBTM_DEBUG_TIMING
+    const auto t0 = std::chrono::steady_clock::now();
+    const int rc = status(cudaLaunchKernelExC(&cfg, kernel, args));
+    g_launch_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+    g_launch_calls += 1;
+    return rc;
+#else
+    return status(cudaLaunchKernelExC(&cfg, kernel, args));
+#endif
 }
 
 inline bool staged(const cbtm_pool *pool) { return (pool->flags & CBTM_POOL_STAGED_LAUNCHES) != 0; }
@@ -288,6 +312,12 @@ int cbtm_sum_reduce(const uint64_t *bits, uint32_t *counters, int depth, void *w
 
 #ifdef CBTM_DEBUG_TIMING
 // debug builds only (benchmarks/reduce_probe.py): per-CTA stamps of the last k_sum_reduce launch
+extern "C" long long cbtm_debug_launch_ns(int reset)
+{
+    const long long avg = g_launch_calls ? g_launch_ns / g_launch_calls : 0;
+    if (reset) g_launch_ns = g_launch_calls = 0;
+    return avg;
+}
 extern "C" int cbtm_debug_probes(unsigned long long *host_out, int reset)
 {
     int rc = status(cudaMemcpyFromSymbol(host_out, g_probe, sizeof(g_probe)));

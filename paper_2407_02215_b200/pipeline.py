@@ -67,9 +67,8 @@ class UpdateStats:
     @classmethod
     def from_device_words(cls, words, epoch: int, times=None) -> "UpdateStats":
         w = words if type(words) is list else [int(x) for x in words]
-        lo = _lib.STAT_PHASE_NS
-        ph = w[lo:lo + _N_PHASES]
-        if times is None and any(ph):
+        ph = w[16:22]   # _lib.STAT_PHASE_NS, six phases
+        if times is None and (ph[0] or ph[1]):
             # device-measured phase times (ns) folded onto the reference's nine stages:
             # t2 cache pointers = index (also resets the commands, stage 3); t4 generate commands =
             # classify + admission + scatter; t5 reserve = agreement + slot hand-out;
@@ -175,7 +174,7 @@ def lod_verdict(state, prm) -> "_lib.CVerdict":
             state._lod_cv = cv  # one struct per state; prm is copied by value at every launch
         except AttributeError:
             pass
-    if isinstance(prm, C.Array):  # LodDecide._prm_c: a ctypes view of the packed parameters
+    if type(prm) is bytes or isinstance(prm, C.Array):  # LodDecide._prm_b: the packed parameters
         C.memmove(cv.prm, prm, 8 * _lib.PRM_WORDS)
     else:
         prm = np.ascontiguousarray(prm, dtype=np.float64)
