@@ -274,6 +274,8 @@ class ParallelEngine:
         if cv is not None and not self.profile and not (self.linger_ns and cv.mode == _lib.VERDICT_LOD):
             # device verdict source: stages 1-9 in one cooperative launch; launch + wait for the
             # frame's counters in ONE call into the library
+            if state.complete_rows:
+                state.complete_rows = False     # (a profiling engine used this state before)
             rc = L.cbtm_update_wait(state.c_pool_ref(), cv, state._stats_host_ptr, 20_000_000_000,
                                     state.stream())
             if rc:

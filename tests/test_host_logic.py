@@ -215,3 +215,29 @@ def test_stats_csv_and_convergence():
     assert (s.epoch, s.live_before, s.live_after, s.splits_applied, s.merges_applied,
             s.splits_rejected_oom, s.merges_rejected_oom, s.split_allocs, s.merge_allocs) == \
         (5, 7, 8, 3, 4, 1, 2, 5, 6)
+
+
+def test_bench_reference_arm_runs_on_cpu_and_prints_the_contract_line():
+    """`bench.py --impl reference` (here: the C port only, a small pool) needs no GPU, runs on rank 0
+    only, and prints ONE JSON line with the keys the driver reads."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    base = [sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--port-only", "--depth", "14",
+            "--steps", "3", "--warmup", "3", "--gpus", "2"]
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    out = subprocess.run(base, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["unit"] == "bisectors/s" and line["higher_is_better"] is True
+    assert line["steps"] == 3 and line["warmup"] == 3 and line["n_gpus"] == 2 and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"] == {"value": line["value"], "unit": "bisectors/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert line["config"]["planets"] == 8 and line["scaling"] == "strong"          # N > 1: BASELINE config 5
+    # every other rank of a torchrun launch exits 0 without work
+    other = subprocess.run(base, cwd=root, env=dict(env, RANK="1", WORLD_SIZE="2"), capture_output=True, text=True, timeout=60)
+    assert other.returncode == 0 and other.stdout.strip() == ""
