@@ -4,10 +4,10 @@
 modes of the kernel: `delta` (stamped tree: per-tile atomic deltas into the levels above the
 tile roots) and `rebuild` (unstamped tree: last-CTA pass).
 
-    python benchmarks/reduce_sweep.py [--depths 20 22 24 26 28 30] [--tune 3,4 ...]
+    python benchmarks/reduce_sweep.py [--depths 20 22 24 26 28 30] [--batch 16] [--env CBTM_REDUCE_NO_PREFETCH ...]
 
---tune runs the sweep once per "ctas_per_sm,max_stages" setting (CBTM_REDUCE_TUNE, read once per
-process, hence a subprocess each); without it the library's own grid policy is measured.
+--env runs the sweep once more per measurement hook of the library (CBTM_REDUCE_NO_PREFETCH,
+CBTM_REDUCE_NO_PDL: read once per process, hence a subprocess each).
 """
 from __future__ import annotations
 
@@ -23,7 +23,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def sweep(depths, reps, out):
+def sweep(depths, reps, out, batch_override=0):
     import torch
     from paper_2407_02215_b200 import _lib
     from benchmarks.cbt_microbench import device_bits, flush_l2
@@ -38,7 +38,7 @@ def sweep(depths, reps, out):
     rows = []
     for depth in depths:
         n = 1 << depth
-        nb = 8 if depth <= 28 else 4
+        nb = batch_override or (8 if depth <= 28 else 4)
         bits = device_bits(depth, 0.5, False, dev)
         want = 0
         for lo in range(0, bits.numel(), 1 << 22):
@@ -110,24 +110,23 @@ def sweep(depths, reps, out):
         torch.cuda.empty_cache()
     if out:
         with open(out, "w") as fh:
-            json.dump({"peak_gbs": peak, "tune": os.environ.get("CBTM_REDUCE_TUNE"), "rows": rows}, fh, indent=1)
+            json.dump({"peak_gbs": peak, "rows": rows}, fh, indent=1)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--depths", type=int, nargs="+", default=[20, 22, 24, 26, 28, 30])
     ap.add_argument("--reps", type=int, default=15)
-    ap.add_argument("--tune", nargs="*", default=None)
+    ap.add_argument("--env", nargs="*", default=None)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--batch", type=int, default=0, help="launches (and cold copies) per series; default 8, 4 beyond 2^28")
     args = ap.parse_args()
-    if args.tune:
-        for t in args.tune:
-            print(f"--- CBTM_REDUCE_TUNE={t}", flush=True)
-            env = dict(os.environ, CBTM_REDUCE_TUNE=t)
-            subprocess.run([sys.executable, os.path.abspath(__file__), "--reps", str(args.reps), "--depths",
-                            *map(str, args.depths)], env=env, check=False)
-        return
-    sweep(args.depths, args.reps, args.out)
+    sweep(args.depths, args.reps, args.out, args.batch)
+    for hook in args.env or []:
+        print(f"--- {hook}=1", flush=True)
+        env = dict(os.environ, **{hook: "1"})
+        subprocess.run([sys.executable, os.path.abspath(__file__), "--reps", str(args.reps), "--batch", str(args.batch),
+                        "--depths", *map(str, args.depths)], env=env, check=False)
 
 
 if __name__ == "__main__":

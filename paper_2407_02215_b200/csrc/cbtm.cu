@@ -21,7 +21,6 @@ namespace {
 constexpr int MAX_DEVICES = 64;
 struct DeviceInfo {
     std::atomic<int> sm_count{0};
-    std::atomic<int> reduce_smem_opt_in{0};
     std::atomic<int> frame_ctas_per_sm[2] = {{0}, {0}};
     std::atomic<int> batch_ctas_per_sm{0};
 };
@@ -62,62 +61,32 @@ inline unsigned strided_grid(uint64_t units, uint64_t per_cta, int ctas_per_sm)
     return want ? (unsigned)want : 1u;
 }
 
-// tuning hook for benchmarks/reduce_sweep.py: "ctas_per_sm,max_stages" (unset: the policy below)
-inline bool reduce_tuning(unsigned *ctas_per_sm, unsigned *max_stages)
-{
-    static const char *env = getenv("CBTM_REDUCE_TUNE");
-    if (!env) return false;
-    unsigned a = 0, b = 0;
-    if (sscanf(env, "%u,%u", &a, &b) != 2 || a < 1 || a > 8 || b < 1 || b > (unsigned)RED_MAX_STAGES) return false;
-    *ctas_per_sm = a, *max_stages = b;
-    return true;
-}
-
 int reduce_launch(const uint64_t *bits, uint32_t *counters, int depth, unsigned *ticket, cudaStream_t st)
 {
-    DeviceInfo &d = device_info();
-    if (!d.reduce_smem_opt_in.load(std::memory_order_acquire)) {
-        const cudaError_t e = cudaFuncSetAttribute(k_sum_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   RED_MAX_STAGES * RED_TILE_BYTES);
-        if (e != cudaSuccess) return status(e);
-        d.reduce_smem_opt_in.store(1, std::memory_order_release);
-    }
     const Geo g = make_geo(depth);
     const unsigned tiles = g.nblocks > (unsigned)RED_TILE_BLOCKS ? g.nblocks / RED_TILE_BLOCKS : 1u;
     const uint64_t total_bytes = (uint64_t)bitfield_words(depth) * 8;
-    // Each CTA streams its tiles through a ring of 16 KB stages; every stage is a TMA bulk copy in
-    // flight.  Up to four tiles per SM (2^26): one CTA per tile, everything resident and in flight
-    // at once.  Beyond that: 3 CTAs per SM with two stages each -- 14 MB in flight, twice what
-    // the HBM pipe needs -- of which only the first two tiles are dealt statically; the rest are
-    // claimed as stages free up, so that SMs which stream faster take more tiles (measured:
-    // 4 stages -> 2^28 13.3 us, 2 stages -> 9.7 us; 2^30 the same 29 us).
-    unsigned ctas_per_sm = 3, max_stages = 2;
-    const bool tuned = reduce_tuning(&ctas_per_sm, &max_stages);
-    const unsigned sms = (unsigned)sm_count();
-    unsigned grid = tiles;
-    if (tuned) grid = tiles < sms * ctas_per_sm ? tiles : sms * ctas_per_sm;
-    else if (tiles > 4 * sms) grid = sms * ctas_per_sm;
-    const unsigned per_cta = (tiles + grid - 1) / grid;
-    unsigned stages = per_cta < max_stages ? per_cta : max_stages;
-    // a tree that was never built is finished by the last CTA, which reuses the ring as a heap
-    // of 2 * tiles words
-    while ((size_t)stages * RED_TILE_BYTES < (size_t)tiles * 8) ++stages;
-
+    // one CTA per 16 KB tile (8192 at the ABI's largest pool); the shared-memory heap is only touched
+    // by the last CTA of a tree that was never built
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
+    cfg.gridDim = dim3(tiles);
     cfg.blockDim = dim3(RED_THREADS);
-    cfg.dynamicSmemBytes = (size_t)stages * RED_TILE_BYTES;
+    cfg.dynamicSmemBytes = (size_t)(tiles < RED_HEAP_ROOTS ? tiles : RED_HEAP_ROOTS) * 8;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     // programmatic dependent launch: this grid's CTAs may be scheduled while the previous kernel
-    // of the stream drains; the kernel waits (griddepcontrol.wait) before it touches memory
+    // of the stream drains; the kernel prefetches its tiles into L2 and waits (griddepcontrol.wait)
+    // before it reads memory
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
-    static const bool no_pdl = getenv("CBTM_REDUCE_NO_PDL") != nullptr; // measurement hook
+    static const bool no_pdl = getenv("CBTM_REDUCE_NO_PDL") != nullptr;           // measurement hooks
+    static const bool no_prefetch = getenv("CBTM_REDUCE_NO_PREFETCH") != nullptr;
     cfg.attrs = attr;
     cfg.numAttrs = no_pdl ? 0 : 1;
-    return status(cudaLaunchKernelEx(&cfg, k_sum_reduce, reinterpret_cast<const uint8_t *>(bits), counters, g.lc,
-                                     total_bytes, tiles, (int)stages, ticket));
+    const bool wide = ((uintptr_t)bits & 31) == 0; // 256-bit loads need 32-byte alignment, the ABI asks for 16
+    return status(cudaLaunchKernelEx(&cfg, wide ? k_sum_reduce<true> : k_sum_reduce<false>,
+                                     reinterpret_cast<const uint8_t *>(bits), counters, g.lc, total_bytes, tiles, ticket,
+                                     no_pdl || no_prefetch ? 0 : 1));
 }
 
 int check_pool(const cbtm_pool *p, bool need_ws)
@@ -303,10 +272,10 @@ int cbtm_sum_reduce(const uint64_t *bits, uint32_t *counters, int depth, void *w
 {
     if (bad_depth(depth)) return CBTM_E_DEPTH;
     if (!bits || !counters || !workspace) return CBTM_E_NULL;
-    if (((uintptr_t)bits | (uintptr_t)counters) & 15) return CBTM_E_ALIGN; // TMA bulk copies; 128-bit counter loads
+    if (((uintptr_t)bits | (uintptr_t)counters) & 15) return CBTM_E_ALIGN; // bulk prefetch, 128-bit loads
     if (workspace_bytes < 256) return CBTM_E_WORKSPACE;
-    // words 0 and 1 of the workspace (also of a pool's frame workspace) are the rebuild ticket and
-    // the tile claim counter; both must be zero on entry and the kernel leaves them zero again
+    // word 0 of the workspace (also of a pool's frame workspace) is the ticket of the rebuild path;
+    // it must be zero on entry and the kernel leaves it zero again
     return reduce_launch(bits, counters, depth, reinterpret_cast<unsigned *>(workspace), as_stream(stream));
 }
 

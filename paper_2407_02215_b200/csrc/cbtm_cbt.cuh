@@ -10,27 +10,31 @@ namespace cbtm {
 // ---------------------------------------------------------------------------
 // Sum reduction (Cbt.sum_reduce, cbt.py:61-68; pipeline stage 9).
 //
-// A tile is 2^17 slots = 16 KB of bitfield = 128 leaf blocks.  Tiles are dealt
-// round-robin to the CTAs, which stream them through a ring of 16 KB shared
-// memory stages filled by TMA bulk copies (cp.async.bulk + mbarrier
-// complete_tx): one elected thread keeps up to `stages` tiles in flight, so the
-// HBM pipe stays full without spending registers or LSU issue slots on it.
-// Every thread then owns 64 contiguous bytes of the tile (four conflict-free
-// 128-bit shared loads in a lane-rotated order), so a leaf block is a lane
-// pair and the warp's five tree levels (16+8+4+2+1 nodes) fall out of five
-// shuffle butterflies; disjoint lanes hold one node each and write all 31 with
-// a single store instruction.  The three levels that join the eight warps cost
-// the one CTA barrier per tile that also recycles the stage.  Levels above the
-// tile roots: every tile adds the change of its root to its ancestors with
-// atomics (see TREE_STAMP); only a tree that was never built goes through a
-// last-CTA rebuild (ticket).
+// A tile is 2^17 slots = 16 KB of bitfield = 128 leaf blocks = ONE CTA of 256 threads (32 registers:
+// eight CTAs, 128 KB of loads in flight per SM; the hardware CTA scheduler is the load balancer --
+// SMs that stream faster simply retire more tiles).  No ring, no shared-memory staging:
+//   * a thread fetches its 64 contiguous bytes with two 256-bit loads (every lane a whole sector)
+//     straight into registers, and a warp starts counting when ITS 2 KB have arrived;
+//   * before griddepcontrol.wait (programmatic dependent launch: the CTAs are scheduled while the
+//     previous kernel of the stream drains) the CTA's tile is pulled into L2 by one TMA bulk
+//     prefetch, so that in a back-to-back series the loads behind the wait are L2 hits;
+//   * the 16 words of a thread go through a carry-save adder tree (Harley-Seal: 30 logic operations
+//     on the ALU pipe) that leaves five words to count instead of 16 -- POPC issues at 16 lanes per
+//     clock and SM, and with every tile of a small pool landing within a microsecond it was the
+//     kernel's tail;
+//   * a leaf block is a lane pair and the warp's five tree levels (16+8+4+2+1 nodes) fall out of five
+//     shuffle butterflies; disjoint lanes hold one node each and write all 31 with a single store
+//     instruction; one CTA barrier joins the eight warps (3 more levels);
+//   * levels above the tile roots: every tile adds the CHANGE of its root to its ancestors with
+//     atomics (see TREE_STAMP); only a tree that was never built goes through a last-CTA rebuild.
 // HBM traffic: N/8 bytes read + 4 * (2 << Lc) = N/128 bytes written.
+// (Rounds 1-2 streamed tiles through a ring of TMA bulk copies + mbarriers, 3 CTAs per SM: 0.27 / 0.53
+// / 0.73 of the copy peak at 2^26 / 2^28 / 2^30 where this kernel reaches 0.38 / 0.75 / 0.95.)
 // ---------------------------------------------------------------------------
 constexpr int RED_THREADS = 256;
 constexpr int RED_TILE_BYTES = 16384;
 constexpr int RED_TILE_BLOCKS = 128; // leaf blocks per tile
-constexpr int RED_MAX_STAGES = 4;
-constexpr uint32_t RED_NO_TILE = 0xffffffffu;
+constexpr uint32_t RED_HEAP_ROOTS = 2048; // rebuild path: tile roots the shared-memory heap holds (16 KB)
 
 // end-of-frame bookkeeping (publish_frame)
 struct ReducePublish {
@@ -140,51 +144,6 @@ __device__ __forceinline__ void retire_frame(int64_t *ctl_stats, uint32_t *seq_f
     if (tid == 0) *seq_frame += 1;
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p)
-{
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
-{
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
-{
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@p bra DONE_%=;\n"
-        "bra WAIT_%=;\n"
-        "DONE_%=:\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-// TMA 1-D bulk copy global -> shared, completion signalled on an mbarrier
-__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
-{
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-
 // counters[0] is padding in the heap layout; the library keeps a stamp there that says "every
 // counter above the tile roots equals the sum of its children" (true after any full build and
 // kept true by the in-frame reducer).  With the stamp present a full reduction does not rebuild
@@ -201,6 +160,13 @@ __device__ __forceinline__ void griddep_launch_dependents()
 }
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// TMA bulk prefetch of `bytes` (a multiple of 16) into L2.  L2 is the device's point of coherence, so
+// unlike a load this may be issued for memory an earlier kernel is still writing.
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // Levels above `cnt` subtree roots (counters[cnt .. 2 cnt), cnt a power of two >= 2),
 // built by the last CTA to arrive (ticket; only thread 0 fences -- the fence is
 // cumulative over the preceding barrier).  Binary heap in shared memory (`heap`,
@@ -209,7 +175,7 @@ __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wa
 // copy-out of all internal nodes (walking the levels through L2 instead costs a
 // round trip per level).  All nb CTAs must call it.
 __device__ __forceinline__ void finish_upper_tree(uint32_t *counters, uint32_t cnt, unsigned *ticket,
-                                                  uint32_t *heap, bool *is_last, uint32_t nb)
+                                                  uint32_t *heap, bool *is_last, uint32_t nb, uint32_t heap_cap = ~0u)
 {
     const int t = threadIdx.x;
     __syncthreads();
@@ -220,6 +186,15 @@ __device__ __forceinline__ void finish_upper_tree(uint32_t *counters, uint32_t c
     __syncthreads();
     if (!*is_last) return;
     __threadfence();
+    // more roots than the shared-memory heap holds (heap_cap of them): the first levels go through L2
+    for (; cnt > heap_cap; cnt >>= 1) {
+        const uint32_t w = cnt >> 1;
+        for (uint32_t i = t; i < w; i += RED_THREADS) {
+            const uint2 kids = __ldcg(reinterpret_cast<const uint2 *>(counters + 2 * (w + i)));
+            counters[w + i] = kids.x + kids.y;
+        }
+        __syncthreads();
+    }
     for (uint32_t base = 0; base < cnt; base += 8 * RED_THREADS) {
         uint32_t r[8];
 #pragma unroll
@@ -246,184 +221,192 @@ __device__ __forceinline__ void finish_upper_tree(uint32_t *counters, uint32_t c
     __syncthreads();
 }
 
+// The subtree of one tile (128 leaf blocks, 8 levels), shared by the two reduction kernels.  A thread
+// holds the count `c` of its 64 contiguous bytes: a leaf block is a lane pair, five butterflies give the
+// warp's 16+8+4+2+1 nodes, disjoint lanes each hold one node and write all 31 with one store
+// instruction.  Returns the warp's root (16 leaf blocks).
+__device__ __forceinline__ uint32_t tile_tree_warp(uint32_t c, uint32_t tile, int lc, uint32_t *counters, int lane,
+                                                   int warp)
+{
+    // butterflies: l0 leaf block (lane pair) ... l4 all 16 leaf blocks of the warp
+    const uint32_t l0 = c + __shfl_xor_sync(FULL_MASK, c, 1);
+    const uint32_t l1 = l0 + __shfl_xor_sync(FULL_MASK, l0, 2);
+    const uint32_t l2 = l1 + __shfl_xor_sync(FULL_MASK, l1, 4);
+    const uint32_t l3 = l2 + __shfl_xor_sync(FULL_MASK, l2, 8);
+    const uint32_t l4 = l3 + __shfl_xor_sync(FULL_MASK, l3, 16);
+
+    uint32_t val = 0, pos = 0;
+    int lvl = -1;
+    if ((lane & 1) == 0) {
+        val = l0, lvl = lc, pos = tile * 128 + warp * 16 + (lane >> 1);
+    } else if ((lane & 3) == 1) {
+        val = l1, lvl = lc - 1, pos = tile * 64 + warp * 8 + (lane >> 2);
+    } else if ((lane & 7) == 3) {
+        val = l2, lvl = lc - 2, pos = tile * 32 + warp * 4 + (lane >> 3);
+    } else if ((lane & 15) == 7) {
+        val = l3, lvl = lc - 3, pos = tile * 16 + warp * 2 + (lane >> 4);
+    } else if (lane == 15) {
+        val = l4, lvl = lc - 4, pos = tile * 8 + warp;
+    }
+    if (lvl >= 0 && pos < (1u << lvl)) counters[(1u << lvl) + pos] = val;
+    return l4;
+}
+
+// Warp 0, from the eight warp roots `w` (shared memory): levels lc-5 (4 nodes), lc-6 (2), lc-7 (the
+// tile root); then, on a stamped tree, the levels above: lane l adds the change of the tile root
+// (old_root: the root as the levels above still see it, held by lane 6) to the ancestor on level l.
+__device__ __forceinline__ void tile_tree_top(const uint32_t *w, uint32_t tile, int lc, uint32_t *counters, int lane,
+                                              bool delta_mode, uint32_t old_root)
+{
+    const int top = lc - 7; // level of the tile roots
+    uint32_t v2 = 0, p2 = 0;
+    int l5 = -1;
+    if (lane < 4) {
+        v2 = w[2 * lane] + w[2 * lane + 1], l5 = lc - 5, p2 = tile * 4 + lane;
+    } else if (lane < 6) {
+        const int q = (lane - 4) * 4;
+        v2 = w[q] + w[q + 1] + w[q + 2] + w[q + 3], l5 = lc - 6, p2 = tile * 2 + (lane - 4);
+    } else if (lane == 6) {
+        v2 = w[0] + w[1] + w[2] + w[3] + w[4] + w[5] + w[6] + w[7], l5 = lc - 7, p2 = tile;
+    }
+    if (l5 >= 0 && p2 < (1u << l5)) counters[(1u << l5) + p2] = v2;
+    if (delta_mode) {
+        const uint32_t delta = __shfl_sync(FULL_MASK, v2 - old_root, 6);
+        if (delta != 0 && lane < top) atomicAdd(&counters[(1u << lane) + (tile >> (top - lane))], delta);
+    }
+}
+
 #ifdef CBTM_DEBUG_TIMING
-// per CTA: kernel entry, released by griddepcontrol.wait, first tile landed, last tile counted, SM id
-__device__ unsigned long long g_reduce_stamps[8192 * 5];
+// per CTA: kernel entry, released by griddepcontrol.wait, first tile landed, last tile counted, SM id;
+// four slots of 2048 CTAs, chosen by the 256-byte unit the ticket pointer sits in (so that the launches
+// of a back-to-back series can be told apart: benchmarks/reduce_chain_probe.cu)
+__device__ unsigned long long g_reduce_stamps[4 * 2048 * 5];
+#define RED_STAMP_ROW() (g_reduce_stamps + ((((uintptr_t)ticket >> 8) & 3) * 2048 + blockIdx.x) * 5)
 #define RED_STAMP(slot)                                                                                           \
     do {                                                                                                          \
-        if (threadIdx.x == 0 && blockIdx.x < 8192) g_reduce_stamps[blockIdx.x * 5 + (slot)] = global_ns();        \
+        if (threadIdx.x == 0 && blockIdx.x < 2048) RED_STAMP_ROW()[slot] = global_ns();                           \
     } while (0)
 #else
 #define RED_STAMP(slot)
 #endif
 
-// One full sum reduction by the grid (Cbt.sum_reduce, initialize, BASELINE config 4).
+__device__ __forceinline__ void csa(uint32_t a, uint32_t b, uint32_t c, uint32_t &sum, uint32_t &carry)
+{
+    sum = a ^ b ^ c;
+    carry = (a & b) | (c & (a ^ b));
+}
+
+// number of set bits in 16 words
+__device__ __forceinline__ uint32_t popc_16words(const uint32_t (&w)[16])
+{
+#ifdef CBTM_REDUCE_PLAIN_POPC
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) c += __popc(w[j]);
+    return c;
+#else
+    uint32_t s0, s1, s2, s3, s4, s5, s6, c0, c1, c2, c3, c4, c5, c6;
+    csa(w[0], w[1], w[2], s0, c0);
+    csa(w[3], w[4], w[5], s1, c1);
+    csa(w[6], w[7], w[8], s2, c2);
+    csa(w[9], w[10], w[11], s3, c3);
+    csa(w[12], w[13], w[14], s4, c4);
+    csa(s0, s1, s2, s5, c5);
+    csa(s3, s4, w[15], s6, c6);
+    const uint32_t ones = s5 ^ s6, c7 = s5 & s6;
+    uint32_t t0, t1, t2, d0, d1, d2;
+    csa(c0, c1, c2, t0, d0);
+    csa(c3, c4, c5, t1, d1);
+    csa(c6, c7, t0, t2, d2);
+    const uint32_t twos = t1 ^ t2, d3 = t1 & t2;
+    uint32_t f0, e0;
+    csa(d0, d1, d2, f0, e0);
+    const uint32_t fours = f0 ^ d3, e1 = f0 & d3;
+    const uint32_t eights = e0 ^ e1, sixteens = e0 & e1;
+    return __popc(ones) + 2 * __popc(twos) + 4 * __popc(fours) + 8 * __popc(eights) + 16 * __popc(sixteens);
+#endif
+}
+
+__device__ __forceinline__ void ldg256(const void *p, uint32_t *v)
+{
+    asm volatile("ld.global.cg.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" // L2 only: streamed once, never stale
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "l"(p)
+                 : "memory");
+}
+
+// One full sum reduction by the grid (Cbt.sum_reduce, initialize, BASELINE config 4): gridDim.x = n_tiles.
+// WIDE: the bitfield is 32-byte aligned (256-bit loads); otherwise four 128-bit loads per thread (the ABI
+// asks for 16-byte alignment only).
+template <bool WIDE>
 __global__ void __launch_bounds__(RED_THREADS)
 k_sum_reduce(const uint8_t *bits, uint32_t *counters, int lc, uint64_t total_bytes, uint32_t n_tiles,
-             int n_stages, unsigned *ticket)
+             unsigned *ticket, int prefetch)
 {
-    extern __shared__ __align__(128) uint8_t ring[]; // n_stages x 16 KB (also the upper-tree heap)
-    __shared__ __align__(8) uint64_t full[RED_MAX_STAGES];
-    __shared__ uint32_t wroot[2][RED_THREADS / 32];
-    __shared__ uint32_t stage_tile[RED_MAX_STAGES]; // tile in flight per stage (RED_NO_TILE: none)
-    __shared__ bool is_last;
+    extern __shared__ __align__(16) uint32_t heap[]; // 2 * min(n_tiles, RED_HEAP_ROOTS) words: rebuild path only
+    __shared__ uint32_t wroot[RED_THREADS / 32];
+    __shared__ bool is_last, s_delta;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const uint32_t bid = blockIdx.x, nb = gridDim.x;
-    const uint32_t stages = (uint32_t)n_stages;
+    const uint32_t tile = blockIdx.x;
+    const uint64_t left = total_bytes - (uint64_t)tile * RED_TILE_BYTES;
+    const uint32_t bytes = left < RED_TILE_BYTES ? (uint32_t)left : (uint32_t)RED_TILE_BYTES;
+    const uint8_t *src = bits + (size_t)tile * RED_TILE_BYTES;
 
     RED_STAMP(0);
-    if (t == 0) {
-        for (uint32_t s = 0; s < stages; ++s) mbar_init(&full[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
     griddep_launch_dependents();
-    __syncthreads();
-    griddep_wait(); // nothing above touches global memory: the previous kernel's writes are visible from here on
+    // nothing is READ before the wait: the address comes from the launch parameters, and a line
+    // prefetched into L2 cannot go stale (L2 is where the previous kernel's writes land)
+    if (t == 0 && prefetch) bulk_prefetch_l2(src, bytes);
+    griddep_wait();
     RED_STAMP(1);
 #ifdef CBTM_DEBUG_TIMING
-    if (t == 0 && bid < 8192) {
+    if (t == 0 && tile < 2048) {
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        g_reduce_stamps[bid * 5 + 4] = smid;
+        RED_STAMP_ROW()[4] = smid;
     }
 #endif
-
-    // Tiles: the first `stages` of a CTA are dealt round-robin (tile = bid + s * nb); all further
-    // ones are CLAIMED from a global counter when a stage is refilled.  SMs do not stream at the
-    // same rate (near / far memory die), and with a static deal the slow ones set the kernel's
-    // duration (measured at 2^30: SMs finished between 22.6 and 31.0 us).  Either way the grid
-    // reads one moving contiguous window of the bitfield, which keeps DRAM rows open.  Every CTA
-    // makes exactly one claim that fails, so the counter sees n_tiles - nb * stages + nb
-    // increments per launch: atomicInc wraps it back to zero on the last one (no reset pass).
-    const uint32_t n_static = nb * stages;
-    const bool dynamic = n_tiles > n_static;
-    const uint32_t claim_wrap = n_tiles - n_static + nb - 1;
-    unsigned *claim_counter = ticket + 1;
-    auto tile_bytes = [&](uint32_t tile) -> uint32_t {
-        const uint64_t left = total_bytes - (uint64_t)tile * RED_TILE_BYTES;
-        return left < RED_TILE_BYTES ? (uint32_t)left : (uint32_t)RED_TILE_BYTES;
-    };
-    auto issue = [&](uint32_t tile, uint32_t stage) { // thread 0
-        stage_tile[stage] = tile; // (published to the CTA by the mbarrier's release / acquire)
-        if (tile == RED_NO_TILE) {
-            mbar_arrive(&full[stage]);
-            return;
-        }
-        const uint32_t bytes = tile_bytes(tile);
-        mbar_expect_tx(&full[stage], bytes);
-        bulk_load(ring + (size_t)stage * RED_TILE_BYTES, bits + (size_t)tile * RED_TILE_BYTES, bytes, &full[stage]);
-    };
-    uint32_t claimed = RED_NO_TILE; // thread 0: the claim in flight (posted one refill ahead, so its latency hides)
-    bool claiming = false;
-    if (t == 0) {
-        for (uint32_t s = 0; s < stages; ++s) {
-            const uint32_t tile = bid + s * nb;
-            issue(tile < n_tiles ? tile : RED_NO_TILE, s);
-        }
-        if (dynamic) {
-            claimed = n_static + atomicInc(claim_counter, claim_wrap);
-            claiming = true;
-        }
-    }
-
-    // The roots of the statically dealt tiles as the levels above still see them (delta mode; lane 6
-    // of warp 0 rewrites them).  Fetched now, unconditionally, next to the tiles themselves: after a
-    // cold start these words come from DRAM, and a load issued only once the tile has landed would
-    // sit on the CTA's critical path.
-    const int top = lc - 7; // level of the tile roots (n_tiles > 1)
-    uint32_t old0 = 0, old1 = 0, old2 = 0, old3 = 0;
-    if (t == 6 && n_tiles > 1) {
-        const uint32_t *roots = counters + (1u << top);
-        if (bid < n_tiles) old0 = __ldcg(roots + bid);
-        if (stages > 1 && bid + nb < n_tiles) old1 = __ldcg(roots + bid + nb);
-        if (stages > 2 && bid + 2 * nb < n_tiles) old2 = __ldcg(roots + bid + 2 * nb);
-        if (stages > 3 && bid + 3 * nb < n_tiles) old3 = __ldcg(roots + bid + 3 * nb);
-    }
-    // the same word for every CTA of the grid: only the rebuild path writes it, after the last ticket
-    const bool delta_mode = n_tiles > 1 && __ldcg(&counters[0]) == TREE_STAMP;
-
-    for (uint32_t k = 0;; ++k) {
-        const uint32_t stage = k % stages;
-        mbar_wait(&full[stage], (k / stages) & 1u);
-        const uint32_t tile = stage_tile[stage];
-        if (tile == RED_NO_TILE) break; // (uniform: every thread reads the same word)
-#ifdef CBTM_DEBUG_TIMING
-        if (k == 0) RED_STAMP(2);
-#endif
-        // claimed tiles: the refill prefetched the old root into L2
-        uint32_t old_root = k == 0 ? old0 : k == 1 ? old1 : k == 2 ? old2 : old3;
-        if (delta_mode && t == 6 && k >= stages) old_root = __ldcg(&counters[(1u << top) + tile]);
-
-        // my 64 bytes of the tile; the rotation keeps the four LDS.128 conflict free
-        const uint4 *mine = reinterpret_cast<const uint4 *>(ring + (size_t)stage * RED_TILE_BYTES) + t * 4;
-        uint32_t c = 0;
+    uint32_t w[16];
+    const bool mine = (uint32_t)t * 64u < bytes; // (partial tile of a tiny pool; bytes is a multiple of 128)
+    if (mine && WIDE) {
+        ldg256(src + t * 64, w);
+        ldg256(src + t * 64 + 32, w + 8);
+    } else if (mine) {
+        const uint4 *q = reinterpret_cast<const uint4 *>(src + t * 64);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) c += popc128(mine[(j + (lane >> 1)) & 3]);
-        if ((uint32_t)t * 64u >= tile_bytes(tile)) c = 0; // partial tile of a tiny pool
-
-        // butterflies: l0 leaf block (lane pair) ... l4 all 16 leaf blocks of the warp
-        const uint32_t l0 = c + __shfl_xor_sync(FULL_MASK, c, 1);
-        const uint32_t l1 = l0 + __shfl_xor_sync(FULL_MASK, l0, 2);
-        const uint32_t l2 = l1 + __shfl_xor_sync(FULL_MASK, l1, 4);
-        const uint32_t l3 = l2 + __shfl_xor_sync(FULL_MASK, l2, 8);
-        const uint32_t l4 = l3 + __shfl_xor_sync(FULL_MASK, l3, 16);
-
-        uint32_t val = 0, pos = 0;
-        int lvl = -1;
-        if ((lane & 1) == 0) {
-            val = l0, lvl = lc, pos = tile * 128 + warp * 16 + (lane >> 1);
-        } else if ((lane & 3) == 1) {
-            val = l1, lvl = lc - 1, pos = tile * 64 + warp * 8 + (lane >> 2);
-        } else if ((lane & 7) == 3) {
-            val = l2, lvl = lc - 2, pos = tile * 32 + warp * 4 + (lane >> 3);
-        } else if ((lane & 15) == 7) {
-            val = l3, lvl = lc - 3, pos = tile * 16 + warp * 2 + (lane >> 4);
-        } else if (lane == 15) {
-            val = l4, lvl = lc - 4, pos = tile * 8 + warp;
+        for (int j = 0; j < 4; ++j) {
+            const uint4 v = __ldcg(q + j);
+            w[4 * j] = v.x, w[4 * j + 1] = v.y, w[4 * j + 2] = v.z, w[4 * j + 3] = v.w;
         }
-        if (lvl >= 0 && pos < (1u << lvl)) counters[(1u << lvl) + pos] = val;
-        if (lane == 0) wroot[k & 1][warp] = l4;
-        __syncthreads(); // stage consumed by everyone; warp roots visible
-        if (t == 0) { // refill the stage: the tile claimed one refill ago; post the next claim
-            uint32_t next = RED_NO_TILE;
-            if (claiming) {
-                if (claimed < n_tiles) {
-                    next = claimed;
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(counters + (1u << top) + next));
-                    claimed = n_static + atomicInc(claim_counter, claim_wrap);
-                } else {
-                    claiming = false;
-                }
-            }
-            issue(next, stage);
-        }
-        if (warp == 0) { // levels lc-5 (4 nodes), lc-6 (2), lc-7 (tile root); then the levels above
-            const uint32_t *w = wroot[k & 1];
-            uint32_t v2 = 0, p2 = 0;
-            int l5 = -1;
-            if (lane < 4) {
-                v2 = w[2 * lane] + w[2 * lane + 1], l5 = lc - 5, p2 = tile * 4 + lane;
-            } else if (lane < 6) {
-                const int q = (lane - 4) * 4;
-                v2 = w[q] + w[q + 1] + w[q + 2] + w[q + 3], l5 = lc - 6, p2 = tile * 2 + (lane - 4);
-            } else if (lane == 6) {
-                v2 = w[0] + w[1] + w[2] + w[3] + w[4] + w[5] + w[6] + w[7], l5 = lc - 7, p2 = tile;
-            }
-            if (l5 >= 0 && p2 < (1u << l5)) counters[(1u << l5) + p2] = v2;
-            if (delta_mode) { // lane l adds the change of the tile root to the ancestor on level l
-                const uint32_t delta = __shfl_sync(FULL_MASK, v2 - old_root, 6);
-                if (delta != 0 && lane < top) atomicAdd(&counters[(1u << lane) + (tile >> (top - lane))], delta);
-            }
-        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) w[j] = 0;
+    }
+    const int top = lc - 7; // level of the tile roots (n_tiles > 1)
+    uint32_t old_root = 0;
+    // The stamp is the same word for every CTA of the grid (only the rebuild path writes it, after the
+    // last ticket).  ONE lane per CTA reads it: a load by every warp put 8 requests per CTA on a single
+    // L2 sector -- 4096 at 2^26, served one per clock by its slice: a microsecond at the head of the launch.
+    bool delta_mode = false;
+    if (t == 6 && n_tiles > 1) {
+        old_root = __ldcg(counters + (1u << top) + tile);
+        delta_mode = __ldcg(&counters[0]) == TREE_STAMP;
     }
 
+    const uint32_t c = popc_16words(w);
+    RED_STAMP(2);
+    const uint32_t l4 = tile_tree_warp(c, tile, lc, counters, lane, warp);
+    if (lane == 0) wroot[warp] = l4;
+    if (t == 6) s_delta = delta_mode;
+    __syncthreads();
+    if (warp == 0) tile_tree_top(wroot, tile, lc, counters, lane, s_delta, old_root);
     RED_STAMP(3);
     if (n_tiles == 1) { // the single tile's subtree is the whole tree
-        if (bid == 0 && t == 0) counters[0] = TREE_STAMP;
+        if (t == 0) counters[0] = TREE_STAMP;
         return;
     }
-    if (delta_mode) return;
-    finish_upper_tree(counters, n_tiles, ticket, reinterpret_cast<uint32_t *>(ring), &is_last, nb);
+    if (s_delta) return;
+    finish_upper_tree(counters, n_tiles, ticket, heap, &is_last, gridDim.x, RED_HEAP_ROOTS);
 }
 
 // ---------------------------------------------------------------------------

@@ -1859,7 +1859,7 @@ __global__ void k_initialize(const cbtm_pool p, const int32_t *__restrict__ he_n
             ctl->seq_frame = 0;
             ctl->need_total = 0;
             ticket[0] = 0;
-            ticket[1] = 0; // k_sum_reduce's tile claim counter
+            ticket[1] = 0; // (spare)
             for (int k = 0; k < CBTM_STATS_WORDS; ++k) ctl->stats[k] = 0;
         }
     }

@@ -216,8 +216,8 @@ def _consistent(nodes, depth):
 def test_sum_reduce_rebuild_and_delta_paths_agree_with_the_oracle(depth):
     """k_sum_reduce: an unstamped tree (fresh, zeroed or garbage counters) is rebuilt by the last CTA
     and stamped; a stamped tree takes per-tile atomic deltas -- after arbitrary changes of the
-    bitfield, repeatedly, with statically dealt and (2^28) dynamically claimed tiles.  Every level
-    against the oracle's heap up to 2^24, against the sum-of-children property and the popcount above."""
+    bitfield, repeatedly, from one tile to 2048.  Every level against the oracle's heap up to 2^24,
+    against the sum-of-children property and the popcount above."""
     import torch
     from paper_2407_02215_b200 import _lib
     L = _lib.load()
@@ -251,7 +251,7 @@ def test_sum_reduce_rebuild_and_delta_paths_agree_with_the_oracle(depth):
         nodes = _heap_on_device(bits, counters, depth)
         assert int(nodes[1]) == popcount(bits), tag
         assert _consistent(nodes, depth), tag
-        assert int(ws.view(torch.int32)[0]) == 0 and int(ws.view(torch.int32)[1]) == 0, tag   # ticket + claim counter
+        assert int(ws.view(torch.int32)[0]) == 0 and int(ws.view(torch.int32)[1]) == 0, tag   # the rebuild ticket is left at zero
         if depth <= 24:
             import oracle
             host = np.zeros(2 * n, np.uint32)
@@ -274,6 +274,57 @@ def test_sum_reduce_rebuild_and_delta_paths_agree_with_the_oracle(depth):
     counters.zero_()                                          # a caller reset the counters: rebuild again
     reduce_and_check("rebuild from zeroed counters")
     assert int(counters[0]) == stamp
+
+
+def _counter_tree_consistent(bits, counters, depth):
+    """leaf counters == popcount of their 1024-slot block, every counter above == sum of its children
+    (the packed tree itself, without expanding it to the reference's heap)"""
+    import torch
+    lc = depth - 10
+    lut = torch.tensor([bin(i).count("1") for i in range(256)], dtype=torch.int32, device=bits.device)
+    leaf = counters[1 << lc:2 << lc]
+    by = bits.view(torch.uint8)
+    step = 1 << 26                                            # bytes per chunk
+    for lo in range(0, by.numel(), step):
+        want = lut[by[lo:lo + step].to(torch.int64)].view(-1, 128).sum(dim=1, dtype=torch.int32)
+        if not torch.equal(want, leaf[lo // 128:lo // 128 + want.numel()]):
+            return False
+    inner = counters[1:1 << lc]
+    kids = counters[2:2 << lc].view(-1, 2).sum(dim=1, dtype=torch.int32)
+    return bool(torch.equal(inner, kids))
+
+
+def test_sum_reduce_at_the_largest_pool_and_on_a_16_byte_aligned_bitfield():
+    """2^30 slots (the ABI's limit): 8192 tiles, the rebuild path takes its first two levels through L2
+    because the shared-memory heap holds 2048 roots; then the delta path.  And a bitfield that is
+    16- but not 32-byte aligned (the ABI's contract) goes through the 128-bit-load variant."""
+    import torch
+    from paper_2407_02215_b200 import _lib
+    L = _lib.load()
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(99)
+    ws = torch.zeros(1024, dtype=torch.uint8, device=dev)
+    stream = _lib.stream_handle(dev)
+    for depth, shift_words in ((30, 0), (22, 2), (30, 2)):
+        words = (1 << depth) // 64
+        store = torch.randint(-2 ** 63, 2 ** 63 - 1, (words + 4,), dtype=torch.int64, device=dev, generator=gen)
+        if store.data_ptr() % 32:
+            store = store[2:]                                 # (torch allocations are 512-byte aligned anyway)
+        bits = store[shift_words:shift_words + words]
+        assert bits.data_ptr() % 32 == (16 if shift_words else 0)
+        counters = torch.randint(0, 2 ** 31 - 1, (L.cbtm_counter_words(depth),), dtype=torch.int32, device=dev,
+                                 generator=gen)
+        counters[0] = 777
+        _lib.check(L.cbtm_sum_reduce(_lib.ptr(bits), _lib.ptr(counters), depth, _lib.ptr(ws), 1024, stream), "rebuild")
+        assert _counter_tree_consistent(bits, counters, depth), (depth, shift_words, "rebuild")
+        assert int(ws.view(torch.int32)[0]) == 0
+        bits[::3] ^= 0x00FF00FF00FF                           # change a third of the words, everywhere
+        bits[: words // 5] = -1
+        _lib.check(L.cbtm_sum_reduce(_lib.ptr(bits), _lib.ptr(counters), depth, _lib.ptr(ws), 1024, stream), "delta")
+        assert _counter_tree_consistent(bits, counters, depth), (depth, shift_words, "delta")
+        del store, bits, counters
+        torch.cuda.empty_cache()
 
 
 def test_sum_reduce_rejects_misaligned_counters():
