@@ -727,21 +727,31 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
             const uint32_t z0 = zline + (zeros_before & 31u);
             uint32_t p1 = o1, p0 = z0;
             if (g.span == 1024u && want_free) { // decode-all: every slot goes to exactly one of the two lists
-                // one select and ONE store per word: the staging index is p1 + r1 for a set bit and
-                // p0 + lane - r1 for a clear one (this loop is bound by instruction issue)
+                // Lane w expands ITS OWN word: one POPC and a five-step scan per block give every word's
+                // first staging index in both lists; then 32 steps of test-bit / select / store / count --
+                // no shuffle and no POPC inside the loop.  (Rounds 1-2 took a word per step across the
+                // lanes -- shuffle, two POPCs on the quarter-rate pipe, twelve instructions per 32 slots --
+                // and were bound by instruction issue: 2^30 leaves 916 us.  Now 864 us; the lanes' staging
+                // addresses are unrelated, so a store takes ~4 bank conflicts and the kernel is bound by
+                // the shared-memory data path: ncu l1tex 91 % of peak, profiles/r3_index_d28_ncu.txt.)
                 const uint32_t own = own_full;
-                uint32_t p0l = p0 + (uint32_t)lane;
-#pragma unroll 8
-                for (int w = 0; w < 32; ++w) {
-                    const uint32_t word = __shfl_sync(FULL_MASK, own, w);
-                    const uint32_t r1 = __popc(word & lane_lt);
-                    const bool bit = (word >> lane) & 1u;
-                    const int32_t slot = base + w * 32 + lane;
-                    st[bit ? p1 + r1 : p0l - r1] = slot;
-                    if (RESET && bit) reset_cmds[slot] = 0u;
-                    const uint32_t c = __popc(word);
-                    p1 += c;
-                    p0l += 32u - c;
+                const uint32_t c = __popc(own);
+                uint32_t incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t up = __shfl_up_sync(FULL_MASK, incl, o);
+                    if (lane >= o) incl += up;
+                }
+                const uint32_t e1 = incl - c; // ones in the words before mine
+                uint32_t q1 = p1 + e1;                                       // next set bit of my word goes here
+                const uint32_t q01 = (p0 + 32u * (uint32_t)lane - e1) + q1;  // a clear bit k goes to q01 + k - q1
+                const int32_t v = base + 32 * lane;
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    const bool bit = (own >> k) & 1u;
+                    st[bit ? q1 : q01 + (uint32_t)k - q1] = v + k;
+                    if (RESET && bit) reset_cmds[v + k] = 0u;
+                    q1 += bit;
                 }
             } else if (g.span == 1024u) { // every word fully valid (all pools with D >= 10)
                 const uint32_t own = own_full;
