@@ -310,8 +310,11 @@ int cbtm_decode_ones(const uint64_t *bits, const uint32_t *counters, int depth, 
     if (K < 0) return CBTM_E_RANGE;
     if (((uintptr_t)bits | (uintptr_t)counters) & 15) return CBTM_E_ALIGN; // 128-bit loads of lines / sibling counters
     if (K == 0) return 0;
-    k_decode<true><<<strided_grid((uint64_t)K, 256, 8), 256, 0, as_stream(stream)>>>(bits, counters, depth,
-                                                                                   ranks, K, out);
+    const unsigned grid = strided_grid((uint64_t)K, 256, 8);
+    if ((((uintptr_t)bits | (uintptr_t)counters) & 31) == 0) // 32-byte aligned: 256-bit loads
+        k_decode<true, true><<<grid, 256, 0, as_stream(stream)>>>(bits, counters, depth, ranks, K, out);
+    else
+        k_decode<true, false><<<grid, 256, 0, as_stream(stream)>>>(bits, counters, depth, ranks, K, out);
     return launch_status();
 }
 
@@ -323,8 +326,11 @@ int cbtm_decode_zeros(const uint64_t *bits, const uint32_t *counters, int depth,
     if (K < 0) return CBTM_E_RANGE;
     if (((uintptr_t)bits | (uintptr_t)counters) & 15) return CBTM_E_ALIGN; // 128-bit loads of lines / sibling counters
     if (K == 0) return 0;
-    k_decode<false><<<strided_grid((uint64_t)K, 256, 8), 256, 0, as_stream(stream)>>>(bits, counters, depth,
-                                                                                    ranks, K, out);
+    const unsigned grid = strided_grid((uint64_t)K, 256, 8);
+    if ((((uintptr_t)bits | (uintptr_t)counters) & 31) == 0)
+        k_decode<false, true><<<grid, 256, 0, as_stream(stream)>>>(bits, counters, depth, ranks, K, out);
+    else
+        k_decode<false, false><<<grid, 256, 0, as_stream(stream)>>>(bits, counters, depth, ranks, K, out);
     return launch_status();
 }
 

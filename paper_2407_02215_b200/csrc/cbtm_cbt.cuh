@@ -532,7 +532,7 @@ k_upper_reduce(const uint64_t *bits, uint8_t *dirty, uint32_t *counters, int lc)
 // descent over the counter heap, then popcount select inside the 128-byte leaf
 // block.
 // ---------------------------------------------------------------------------
-template <bool ONES>
+template <bool ONES, bool WIDE = false>
 __device__ __forceinline__ int32_t cbt_find(const uint64_t *bits, const uint32_t *counters,
                                             const Geo &g, uint32_t rank)
 {
@@ -543,10 +543,18 @@ __device__ __forceinline__ int32_t cbt_find(const uint64_t *bits, const uint32_t
     // dependent load per three levels instead of three.
     for (; l + 3 <= g.lc; l += 3) {
         const uint32_t base = node << 3;
-        const uint4 lo = *reinterpret_cast<const uint4 *>(counters + base);
-        const uint4 hi = *reinterpret_cast<const uint4 *>(counters + base + 4);
+        uint32_t c[8];
+        if (WIDE) { // 32-byte aligned counters: the eight siblings with one load instruction
+            asm volatile("ld.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(c[4]), "=r"(c[5]), "=r"(c[6]), "=r"(c[7])
+                         : "l"(counters + base)
+                         : "memory");
+        } else {
+            const uint4 lo = *reinterpret_cast<const uint4 *>(counters + base);
+            const uint4 hi = *reinterpret_cast<const uint4 *>(counters + base + 4);
+            c[0] = lo.x, c[1] = lo.y, c[2] = lo.z, c[3] = lo.w, c[4] = hi.x, c[5] = hi.y, c[6] = hi.z, c[7] = hi.w;
+        }
         const uint32_t span = (uint32_t)(g.n >> (l + 3)); // slots under each of the eight
-        const uint32_t c[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
         uint32_t k = 0;
 #pragma unroll
         for (int q = 0; q < 7; ++q) {
@@ -569,9 +577,47 @@ __device__ __forceinline__ int32_t cbt_find(const uint64_t *bits, const uint32_t
         half >>= 1;
     }
     const uint32_t block = node - g.nblocks;
+    const uint64_t *line = bits + (size_t)block * 16;
+    if (WIDE && g.span == 1024u) {
+        // A 32-byte sector per step with one 256-bit load (the bitfield is 32-byte aligned): with
+        // random ranks every lane of a load touches its own line, so the L1 pays per INSTRUCTION and
+        // lane -- a word per step meant 8 loads for the average rank, a sector per step means 2.5
+        // for the same sectors from L2.
+        for (int sct = 0; sct < 4; ++sct) {
+            uint32_t w[8];
+            asm volatile("ld.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                         : "l"(line + 4 * sct)
+                         : "memory");
+            if (!ONES) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) w[j] = ~w[j];
+            }
+            uint32_t c[8], total = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                c[j] = __popc(w[j]);
+                total += c[j];
+            }
+            if (rank >= total) {
+                rank -= total;
+                continue;
+            }
+            uint32_t word = 0, at = 0; // the 32-bit word holding the rank, found without branching
+            bool found = false;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const bool here = !found && rank < c[j];
+                if (here) word = w[j], at = (uint32_t)j;
+                found |= here;
+                if (!found) rank -= c[j];
+            }
+            return (int32_t)(block * 1024u + (uint32_t)sct * 256u + at * 32u + (uint32_t)select32(word, (int)rank));
+        }
+        return -1; // rank out of range
+    }
     // (words are fetched one by one with an early exit: fetching the whole 128-byte line at once costs
     // four times the L2 sectors and made random decodes 1.5x slower)
-    const uint64_t *line = bits + (size_t)block * 16;
     const int words = g.span >= 64 ? (int)(g.span >> 6) : 1;
     for (int w = 0; w < words; ++w) {
         uint64_t x = line[w];
@@ -586,7 +632,8 @@ __device__ __forceinline__ int32_t cbt_find(const uint64_t *bits, const uint32_t
     return -1; // rank out of range
 }
 
-template <bool ONES>
+// WIDE: bitfield and counters are 32-byte aligned (256-bit loads in the descent and in the leaf search)
+template <bool ONES, bool WIDE>
 __global__ void __launch_bounds__(256)
 k_decode(const uint64_t *__restrict__ bits, const uint32_t *__restrict__ counters, int depth,
          const int64_t *__restrict__ ranks, int64_t K, int32_t *__restrict__ out)
@@ -597,7 +644,7 @@ k_decode(const uint64_t *__restrict__ bits, const uint32_t *__restrict__ counter
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = ranks ? ranks[i] : i;
-        out[i] = (r < 0 || (uint64_t)r >= limit) ? -1 : cbt_find<ONES>(bits, counters, g, (uint32_t)r);
+        out[i] = (r < 0 || (uint64_t)r >= limit) ? -1 : cbt_find<ONES, WIDE>(bits, counters, g, (uint32_t)r);
     }
 }
 

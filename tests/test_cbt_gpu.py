@@ -323,6 +323,21 @@ def test_sum_reduce_at_the_largest_pool_and_on_a_16_byte_aligned_bitfield():
         bits[: words // 5] = -1
         _lib.check(L.cbtm_sum_reduce(_lib.ptr(bits), _lib.ptr(counters), depth, _lib.ptr(ws), 1024, stream), "delta")
         assert _counter_tree_consistent(bits, counters, depth), (depth, shift_words, "delta")
+        if shift_words:
+            # ranked decode: the 16-byte aligned bitfield takes the word-by-word leaf search, an aligned
+            # copy the sector-by-sector one (256-bit loads) -- same slots
+            twin = bits.clone()
+            assert twin.data_ptr() % 32 == 0
+            ones = int(counters[1])
+            for fn, limit in ((L.cbtm_decode_ones, ones), (L.cbtm_decode_zeros, (1 << depth) - ones)):
+                ranks = torch.randint(0, limit, (1 << 16,), dtype=torch.int64, device=dev, generator=gen)
+                ranks[:2] = torch.tensor([0, limit - 1], device=dev)
+                a = torch.empty(ranks.numel(), dtype=torch.int32, device=dev)
+                b = torch.empty_like(a)
+                _lib.check(fn(_lib.ptr(bits), _lib.ptr(counters), depth, _lib.ptr(ranks), ranks.numel(), _lib.ptr(a), stream), "decode")
+                _lib.check(fn(_lib.ptr(twin), _lib.ptr(counters), depth, _lib.ptr(ranks), ranks.numel(), _lib.ptr(b), stream), "decode")
+                assert torch.equal(a, b) and int(a.min()) >= 0
+            del twin
         del store, bits, counters
         torch.cuda.empty_cache()
 
