@@ -468,6 +468,7 @@ def run_gpu_earth(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         start_host = state.to_host()
     e2e_state = state.clone()
+    draw_state = state.clone() if rank == 0 and not args.no_draw_leg else None
 
     # ---- device-timed run: K frames, parameters resident, no host sync ----
     L = _lib.load()
@@ -506,9 +507,41 @@ def run_gpu_earth(args):
     e2e_state.synchronize()
     barrier()
     e2e_s = time.perf_counter() - t0
-    clocks = sampler.stop() if rank == 0 else None
     if e2e_rows != [tuple(int(x) for x in rows[j, :8]) for j in range(K)]:
         raise SystemExit("bench.py: e2e run and device-timed run report different counters (parity failure)")
+
+    # ---- the paper's frame: update, then everything a draw call needs ----
+    # Every frame: update as above, then cbtm_export_live_triangles on the same stream (index of the NEW
+    # state, fp64 decode of every live bisector into a device vertex buffer, indirect draw arguments
+    # written on the device).  Shows that other GPU work runs between the frame kernels: update()
+    # returns when the frame's counters are decided, the export is queued behind the rest of the frame.
+    draw = None
+    if rank == 0 and not args.no_draw_leg:
+        cap = 1 << 18
+        vbuf = torch.empty((cap, 3, 3), dtype=torch.float64, device=device)
+        dargs = torch.zeros(4, dtype=torch.int32, device=device)
+        dpool = draw_state.c_pool()
+
+        def frame(j):
+            s = eng.update(draw_state, LodDecide(seq.config, cams[j], seq.mesh), epoch=j)
+            _lib.check(L.cbtm_export_live_triangles(C.byref(dpool), _lib.ptr(draw_state.d_root_tris), _lib.ptr(vbuf), cap,
+                                                    _lib.ptr(dargs), draw_state.stream()), "cbtm_export_live_triangles")
+            return s
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        for j in range(K):
+            s = frame(j)
+        draw_state.synchronize()
+        draw_s = time.perf_counter() - t0
+        if int(dargs[0]) != 3 * s.live_after or s.live_after != int(rows[K - 1, 7]):
+            raise SystemExit("bench.py: draw arguments of the last frame do not match its live count")
+        draw = {"ms_per_step": 1e3 * draw_s / K, "value": units / draw_s, "unit": UNIT,
+                "vertex_buffer_bytes_last_frame": 72 * s.live_after,
+                "mode": "per frame: ParallelEngine().update(...) then cbtm_export_live_triangles (k_index of the new "
+                        "state + fp64 decode of all live bisectors + indirect draw args, device resident) on the same "
+                        "stream; wall clock over K frames including the drain"}
+        del vbuf
+    clocks = sampler.stop() if rank == 0 else None
 
     # ---- max over ranks ----
     t = torch.tensor([gpu_ms, e2e_s * 1e3, float(units)], dtype=torch.float64, device=device)
@@ -614,6 +647,7 @@ def run_gpu_earth(args):
                         "the next frame overlaps with the rest of this one"},
         # persistent path: ONE cooperative launch (k_frames) runs all K frames, six phases each;
         # staged path: index, classify, admit, scatter, agree, reserve, apply, upper_reduce, publish per frame
+        "e2e_update_plus_draw_export": draw,
         "gpu_launches": 9 * K if args.staged else 1,
         "launch_mode": "staged" if args.staged else "persistent (1 cooperative launch, 6 phases x K frames); e2e: K launches",
         "roofline": roofline,
@@ -811,6 +845,7 @@ def main():
     ap.add_argument("--port-only", action="store_true", help="CPU legs: only the C port, not the real reference")
     ap.add_argument("--no-config2", action="store_true")
     ap.add_argument("--no-config4", action="store_true")
+    ap.add_argument("--no-draw-leg", action="store_true", help="skip the update + triangle export leg")
     ap.add_argument("--torchrun-world1", action="store_true",
                     help="run under torch.distributed.run even at N = 1 (exercises NCCL init + the gather)")
     ap.add_argument("--staged", action="store_true",
