@@ -20,3 +20,13 @@ for TOOL in memcheck racecheck synccheck; do
   echo "$TOOL cbt rc=$?" | tee -a $OUT/${TAG}_sanitize_summary.txt
 done
 grep -h "ERROR SUMMARY\|RACECHECK SUMMARY\|passed\|failed\|smoke ok" $OUT/${TAG}_sanitize_*.log | tee -a $OUT/${TAG}_sanitize_summary.txt
+# wider pass (memcheck + racecheck): every update path of the frame kernels (pressure / admission tail, staged launches,
+# batch kernel, linger mode, begin/finish split), the mesh ingest and the API tests
+if [ "${2:-}" = wide ]; then
+  for TOOL in memcheck racecheck; do
+    timeout 3000 $SAN --tool $TOOL --error-exitcode 9 --print-limit 20 python -m pytest tests/test_update_gpu.py tests/test_api_gpu.py \
+        tests/test_mesh_gpu.py -x -q > $OUT/${TAG}_sanitize_${TOOL}_update.log 2>&1
+    echo "$TOOL update/api/mesh rc=$?" | tee -a $OUT/${TAG}_sanitize_summary.txt
+    tail -3 $OUT/${TAG}_sanitize_${TOOL}_update.log | tee -a $OUT/${TAG}_sanitize_summary.txt
+  done
+fi

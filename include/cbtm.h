@@ -50,7 +50,8 @@ extern "C" {
 #define CBTM_E_WORKSPACE 3 /* workspace smaller than cbtm_workspace_bytes */
 #define CBTM_E_MODE 4      /* unknown verdict mode / flag */
 #define CBTM_E_RANGE 5     /* count / size argument out of range */
-#define CBTM_E_ALIGN 6     /* bits, counters, reserved, cache_live, cache_free must be 16-byte aligned */
+#define CBTM_E_ALIGN 6     /* bits, counters, reserved, cache_live, cache_free must be 16-byte aligned
+                              (32-byte aligned bits / counters select the 256-bit-load kernel variants) */
 #define CBTM_E_TIMEOUT 7   /* cbtm_wait_frame gave up */
 
 /* command-word bits (state.py:17-25) */

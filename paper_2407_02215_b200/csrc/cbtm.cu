@@ -21,6 +21,7 @@ namespace {
 constexpr int MAX_DEVICES = 64;
 struct DeviceInfo {
     std::atomic<int> sm_count{0};
+    std::atomic<int> index_all_smem_opt_in{0};
     std::atomic<int> frame_ctas_per_sm[2] = {{0}, {0}};
     std::atomic<int> batch_ctas_per_sm{0};
 };
@@ -341,6 +342,18 @@ int cbtm_index(const uint64_t *bits, const uint32_t *counters, int depth, int32_
     if (!bits || !counters || !cache_live) return CBTM_E_NULL;
     if (((uintptr_t)bits | (uintptr_t)counters | (uintptr_t)cache_live | (uintptr_t)cache_free) & 15) return CBTM_E_ALIGN;
     const Geo g = make_geo(depth);
+    if (cache_free && g.span == 1024u) { // decode-all: double-buffered staging, TMA bulk stores
+        DeviceInfo &d = device_info();
+        if (!d.index_all_smem_opt_in.load(std::memory_order_acquire)) {
+            const cudaError_t e = cudaFuncSetAttribute(k_index_all, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)IDX_ALL_SMEM);
+            if (e != cudaSuccess) return status(e);
+            d.index_all_smem_opt_in.store(1, std::memory_order_release);
+        }
+        k_index_all<<<strided_grid(g.nblocks, IDX_WARPS, 3), IDX_WARPS * 32, IDX_ALL_SMEM, as_stream(stream)>>>(
+            reinterpret_cast<const uint32_t *>(bits), counters, depth, cache_live, cache_free, dispatch);
+        return launch_status();
+    }
     k_index<false><<<strided_grid(g.nblocks, IDX_WARPS, 6), IDX_WARPS * 32, 0, as_stream(stream)>>>(
         reinterpret_cast<const uint32_t *>(bits), counters, depth, cache_live, cache_free, dispatch, nullptr);
     return launch_status();

@@ -653,19 +653,19 @@ k_decode(const uint64_t *__restrict__ bits, const uint32_t *__restrict__ counter
 // stream compaction.  One warp per 1024-slot leaf block:
 //   * its rank offset comes from the counter heap (sum of the left siblings on
 //     the root path -- all addresses known up front, one load per lane);
-//   * lane l owns word l of the block; the warp walks the 32 words, each
-//     broadcast with one shuffle, and lane l handles BIT l of the current word:
-//     its rank inside the word is a popcount under a lane mask, the running
-//     rank is warp-uniform arithmetic -- no data-dependent loops, ~12
-//     instructions per 32 slots.  Slots go to a shared staging area (set bits
-//     first, unset bits behind them), each list placed so that its staging
-//     index is congruent to its global index modulo 32;
+//   * lane l owns word l of the block.  Live list only (the frame's index phase, sparse pools): the
+//     warp walks the non-empty words, each broadcast with one shuffle, and lane l handles BIT l of the
+//     current word -- its rank inside the word is a popcount under a lane mask.  Both lists
+//     (decode-all): every lane expands ITS OWN word, 32 steps of test-bit / select / store / count
+//     from the staging indices a five-step scan of the words' popcounts gives it.  Slots go to a
+//     shared staging area (set bits first, unset bits behind them), each list placed so that its
+//     staging index is congruent to its global index modulo 32;
 //   * the copy-out therefore moves 128-byte-aligned lines with 128-bit shared
 //     loads and 128-bit global stores (scalar stores only on the two edge
 //     vectors of a list).
-// ncu on the first versions showed this kernel bound by instruction issue
-// (71-77 % issue slots busy at ~3.3 TB/s), not by HBM (a bare write stream
-// reaches 6-7 TB/s here), hence the instruction diet.
+// ncu on the first versions showed decode-all bound by instruction issue (71-78 % issue slots busy):
+// hence the instruction diet; the own-word expansion is bound by the shared-memory data path instead
+// (its scattered staging stores take ~4 bank conflicts each).
 // Blocks with no set bit are skipped from their counter without touching the
 // bitfield when the free list is not requested; so are empty words.
 // Plain (coherent) loads only: inside the persistent frame kernel the bitfield
@@ -694,6 +694,33 @@ __device__ __forceinline__ void copy_out_lines(int32_t *out, uint32_t gbase, uin
     }
 }
 
+// The same copy by the TMA: the 16-byte aligned interior of the run as ONE bulk copy shared -> global
+// (cp.async.bulk.global.shared::cta, issued by lane 0), at most three head and three tail entries by
+// scalar stores.  The staging stores must have been made visible to the async proxy
+// (fence.proxy.async + __syncwarp) before the call; the staging area may be rewritten only after
+// cp.async.bulk.wait_group.read says the copy has read it.  Takes the 128-bit shared loads and global stores of the copy-out off the
+// LSU / shared-memory path, which is what bounds decode-all.
+__device__ __forceinline__ void bulk_copy_out(int32_t *out, uint32_t gbase, uint32_t off, uint32_t count,
+                                              const int32_t *st, int lane)
+{
+    const uint32_t end = off + count;
+    const uint32_t a0 = (off + 3u) & ~3u, a1 = end & ~3u; // aligned interior [a0, a1)
+    if (a1 > a0) {
+        if (lane == 0)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + gbase + a0),
+                         "r"((uint32_t)__cvta_generic_to_shared(st + a0)), "r"(4u * (a1 - a0))
+                         : "memory");
+        // head [off, a0) and tail [a1, end): lanes 1..3 and 4..6
+        if (lane >= 1 && lane <= 3 && off + (uint32_t)(lane - 1) < a0) out[gbase + off + (lane - 1)] = st[off + (lane - 1)];
+        if (lane >= 4 && lane <= 6 && a1 + (uint32_t)(lane - 4) < end) out[gbase + a1 + (lane - 4)] = st[a1 + (lane - 4)];
+    } else if ((uint32_t)lane < count) { // fewer than four aligned entries: at most six in all
+        out[gbase + off + lane] = st[off + lane];
+    }
+}
+__device__ __forceinline__ void bulk_copy_out_commit(int lane)
+{
+    if (lane == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 // out[first .. first + count) = slot0, slot0 + 1, ... (a block that is entirely live or free)
 __device__ __forceinline__ void fill_run_lines(int32_t *out, uint32_t first, uint32_t count, int32_t slot0,
                                                int lane)
@@ -712,7 +739,11 @@ __device__ __forceinline__ void fill_run_lines(int32_t *out, uint32_t first, uin
     }
 }
 
-template <bool RESET>
+// BULK (k_index_all): the copy-out of decode-all goes through TMA bulk stores out of TWO staging areas per
+// warp (stage[2 * warp], stage[2 * warp + 1]), so that the store of one block overlaps the expansion of the
+// next.  Standalone kernel only: the stores are awaited when the warp is done, nothing orders them against
+// a later phase of a persistent kernel.
+template <bool RESET, bool BULK = false>
 __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32_t *counters, int depth,
                                             int32_t *cache_live, int32_t *cache_free, uint32_t *dispatch,
                                             uint32_t *reset_cmds, int32_t (*stage)[IDX_STAGE_WORDS],
@@ -724,7 +755,8 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
     const uint32_t nwarps = nb * IDX_WARPS;
     const uint32_t lane_lt = (1u << lane) - 1u;
     const bool want_free = cache_free != nullptr;
-    int32_t *st = stage[warp];
+    int32_t *st = stage[BULK ? 2 * warp : warp];
+    uint32_t bulk_turn = 0; // BULK: staging area of the next block
 
     if (dispatch && bid == 0 && threadIdx.x == 0) {
         const uint32_t n = counters[1];
@@ -748,6 +780,7 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
             const uint32_t cnt = __shfl_sync(FULL_MASK, my_cnt, src);
 
             // the block's bits travel together with the root path (one round trip, not two)
+            // (issuing them one block ahead was measured and rejected: more registers, decode-all 4 % slower)
             const uint32_t own_full = (g.span == 1024u && cnt != 0 && cnt != g.span) ? bits32[(size_t)b * 32 + lane] : 0u;
             // ones before this block: left siblings along the root path
             uint32_t part = 0;
@@ -835,6 +868,20 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
                     p0 += valid - c;
                 }
             }
+            if (BULK && want_free && g.span == 1024u) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); // my staging stores -> async proxy
+                __syncwarp();
+                bulk_copy_out(cache_live, ones_before - o1, o1, cnt, st, lane);
+                bulk_copy_out(cache_free, zeros_before - (zeros_before & 31u), zeros_before & 31u, zcnt, st + zline, lane);
+                bulk_copy_out_commit(lane);
+                // the next block expands into the other staging area, once the store issued from it two
+                // blocks ago has read it (at most one group -- this block's -- stays pending)
+                bulk_turn ^= 1u;
+                st = stage[2 * warp + bulk_turn];
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                __syncwarp();
+                continue;
+            }
             __syncwarp();
             copy_out_lines(cache_live, ones_before - o1, o1, cnt, st, lane);
             if (want_free) copy_out_lines(cache_free, zeros_before - (zeros_before & 31u), zeros_before & 31u, zcnt,
@@ -842,6 +889,7 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
             __syncwarp();
         }
     }
+    if (BULK && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); // writes done before the warp exits
 }
 
 template <bool RESET>
@@ -852,6 +900,18 @@ k_index(const uint32_t *bits32, const uint32_t *counters, int depth, int32_t *ca
     __shared__ __align__(16) int32_t stage[IDX_WARPS][IDX_STAGE_WORDS];
     index_phase<RESET>(bits32, counters, depth, cache_live, cache_free, dispatch, reset_cmds, stage, blockIdx.x,
                        gridDim.x);
+}
+
+// decode-all (both lists, pools of >= 1024 slots): two staging areas per warp, copy-out by TMA bulk
+// stores that overlap the expansion of the warp's next block
+constexpr size_t IDX_ALL_SMEM = sizeof(int32_t) * 2 * IDX_WARPS * IDX_STAGE_WORDS;
+__global__ void __launch_bounds__(IDX_WARPS * 32)
+k_index_all(const uint32_t *bits32, const uint32_t *counters, int depth, int32_t *cache_live, int32_t *cache_free,
+            uint32_t *dispatch)
+{
+    extern __shared__ __align__(128) int32_t stage_dyn[];
+    index_phase<false, true>(bits32, counters, depth, cache_live, cache_free, dispatch, nullptr,
+                             reinterpret_cast<int32_t(*)[IDX_STAGE_WORDS]>(stage_dyn), blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
