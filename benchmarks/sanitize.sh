@@ -9,7 +9,7 @@
 # oracle) and the CBT kernel tests (reduce rebuild + delta up to 2^21, decode, index).
 set -u
 OUT=gpurun_out
-TAG=${1:-r3}
+TAG=${1:-r2b}
 SAN=/usr/local/cuda/bin/compute-sanitizer
 for TOOL in memcheck racecheck synccheck; do
   timeout 900 $SAN --tool $TOOL --error-exitcode 9 --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" \

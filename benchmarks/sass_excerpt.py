@@ -1,9 +1,9 @@
 #!/usr/bin/env python
 """SASS evidence for profiles/: instruction-class counts per kernel of libcbtm.so and the lines that
-prove the mechanisms (TMA bulk copies + mbarriers in k_sum_reduce, programmatic dependent launch,
-atomics / reductions and the fp64 classifier in the frame kernels).
+prove the mechanisms (256-bit loads, TMA bulk prefetch into L2 and programmatic dependent launch in
+k_sum_reduce, TMA bulk stores in k_index_all, atomics / reductions and the fp64 classifier in the frame kernels).
 
-    python benchmarks/sass_excerpt.py > profiles/r2_sass_excerpt.txt
+    python benchmarks/sass_excerpt.py > profiles/r2b_sass_excerpt.txt
 """
 import collections
 import os
@@ -26,8 +26,8 @@ for line in sass.splitlines():
         kernels[cur].append(line)
 demangle = subprocess.run(["c++filt"], input="\n".join(kernels), capture_output=True, text=True).stdout.splitlines()
 names = dict(zip(kernels, demangle))
-CLASSES = ["UBLKCP", "SYNCS", "ACQBULK", "ATOMG", "ATOMS", "REDG", "RED.", "ATOM.", "DADD", "DMUL", "DFMA", "DSETP", "MUFU.RCP64H", "MUFU.RSQ64H",
-           "POPC", "SHFL", "VOTE", "MATCH", "BAR.SYNC", "LDG", "STG", "LDS", "STS", "CCTL", "MEMBAR", "ERRBAR", "UTMALDG", "UTCHMMA", "HMMA"]
+CLASSES = ["UBLKCP", "UBLKPF", "SYNCS", "ACQBULK", "ATOMG", "ATOMS", "REDG", "RED.", "ATOM.", "DADD", "DMUL", "DFMA", "DSETP", "MUFU.RCP64H", "MUFU.RSQ64H",
+           "POPC", "LOP3", "SHFL", "VOTE", "MATCH", "BAR.SYNC", "LDG.E.ENL2.256", "LDG", "STG", "LDS", "STS", "CCTL", "MEMBAR", "ERRBAR", "UTMALDG", "UTCHMMA", "HMMA"]
 
 
 def mnemonic(line):
@@ -49,12 +49,13 @@ for k, lines in kernels.items():
         shown += f" ({no_return} of the ATOMG write no result: destination RZ, fire and forget like REDG)"
     print(f"{nm.split('(')[0]}: {len(ops)} instructions; {shown}")
 
-for want, pats in (("k_sum_reduce", ("UBLKCP", "SYNCS", "ACQBULK", "ATOM", "RED", "PREEXIT", "ACQ", "CCTL.IVALL", "POPC")),):
+for want, pats in (("k_sum_reduce<true>", ("UBLKPF", "ACQBULK", "ATOM", "RED", "PREEXIT", "LDG", "POPC", "CCTL")),
+                   ("k_index_all", ("UBLKCP", "FENCE", "DEPBAR", "LDG"))):
     for k, lines in kernels.items():
         if want in names.get(k, k):
-            print(f"\n## {names[k].split('(')[0]}: TMA bulk copy, mbarrier, dependent-launch and atomic instructions")
+            print(f"\n## {names[k].split('(')[0]}: loads, TMA bulk, dependent-launch, atomic and POPC instructions")
             for l in lines:
-                if any(p in l for p in pats if p != "POPC"):
+                if any(p in l for p in pats):
                     print("   " + l.strip()[:140])
 
 # where the DFMAs of the frame kernel sit: only inside the expansions of __ddiv_rn / __dsqrt_rn / sin

@@ -28,7 +28,7 @@ namespace cbtm {
 //   * levels above the tile roots: every tile adds the CHANGE of its root to its ancestors with
 //     atomics (see TREE_STAMP); only a tree that was never built goes through a last-CTA rebuild.
 // HBM traffic: N/8 bytes read + 4 * (2 << Lc) = N/128 bytes written.
-// (Rounds 1-2 streamed tiles through a ring of TMA bulk copies + mbarriers, 3 CTAs per SM: 0.27 / 0.53
+// (Earlier versions streamed tiles through a ring of TMA bulk copies + mbarriers, 3 CTAs per SM: 0.27 / 0.53
 // / 0.73 of the copy peak at 2^26 / 2^28 / 2^30 where this kernel reaches 0.38 / 0.75 / 0.95.)
 // ---------------------------------------------------------------------------
 constexpr int RED_THREADS = 256;
@@ -357,6 +357,8 @@ k_sum_reduce(const uint8_t *bits, uint32_t *counters, int lc, uint64_t total_byt
     // nothing is READ before the wait: the address comes from the launch parameters, and a line
     // prefetched into L2 cannot go stale (L2 is where the previous kernel's writes land)
     if (t == 0 && prefetch) bulk_prefetch_l2(src, bytes);
+    // (prefetching the two counter words of the delta path as well was measured and rejected: the stamp is
+    // one line for the whole grid, and 8192 prefetches of it cost more than its one cold read)
     griddep_wait();
     RED_STAMP(1);
 #ifdef CBTM_DEBUG_TIMING
@@ -809,11 +811,11 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
             if (g.span == 1024u && want_free) { // decode-all: every slot goes to exactly one of the two lists
                 // Lane w expands ITS OWN word: one POPC and a five-step scan per block give every word's
                 // first staging index in both lists; then 32 steps of test-bit / select / store / count --
-                // no shuffle and no POPC inside the loop.  (Rounds 1-2 took a word per step across the
+                // no shuffle and no POPC inside the loop.  (Earlier versions took a word per step across the
                 // lanes -- shuffle, two POPCs on the quarter-rate pipe, twelve instructions per 32 slots --
                 // and were bound by instruction issue: 2^30 leaves 916 us.  Now 864 us; the lanes' staging
                 // addresses are unrelated, so a store takes ~4 bank conflicts and the kernel is bound by
-                // the shared-memory data path: ncu l1tex 91 % of peak, profiles/r3_index_d28_ncu.txt.)
+                // the shared-memory data path: ncu l1tex 91 % of peak, profiles/r2b_index_own_word_d28_ncu.txt.)
                 const uint32_t own = own_full;
                 const uint32_t c = __popc(own);
                 uint32_t incl = c;
