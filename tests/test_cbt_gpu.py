@@ -91,6 +91,33 @@ def test_pool_like_and_large_pools():
         assert np.array_equal(c.one_to_bit_ids(ranks), oracle.decode_ones(ref, 1 << depth, ranks))
 
 
+def test_index_both_lists_on_nearly_empty_and_nearly_full_blocks():
+    """k_index_all: lists of a block with 0..7 entries (no 16-byte aligned interior for the bulk store: head and
+    tail entries go by scalar stores), next to full, empty and half-full blocks, at every alignment."""
+    depth = 20
+    n = 1 << depth
+    rng = np.random.default_rng(2024)
+    leaves = np.zeros(n, np.uint32)
+    for b in range(n // 1024):
+        kind = b % 6
+        blk = leaves[b * 1024:(b + 1) * 1024]
+        if kind == 0:
+            blk[rng.choice(1024, rng.integers(0, 8), replace=False)] = 1          # 0..7 live slots
+        elif kind == 1:
+            blk[:] = 1
+            blk[rng.choice(1024, rng.integers(0, 8), replace=False)] = 0          # 0..7 free slots
+        elif kind == 2:
+            blk[:] = rng.random(1024) < 0.5
+        elif kind == 3:
+            blk[:] = 1
+        elif kind == 5:
+            blk[rng.integers(0, 1024)] = 1
+    c = make(depth, leaves)
+    live, free = c.index()
+    assert np.array_equal(live, np.flatnonzero(leaves))
+    assert np.array_equal(free, np.flatnonzero(leaves == 0))
+
+
 # -- drop-in behaviour of the class (reference tests/test_cbt.py) ---------------
 
 def test_depth_bounds():
