@@ -68,6 +68,14 @@
         __syncthreads();                                                                                 \
         if (threadIdx.x == 0) atomicMax(&cbtm::g_probe[cbtm::probe_frame() & (PROBE_FRAMES - 1)][slot], cbtm::probe_now()); \
     } while (0)
+// per warp, no CTA barrier (usable in divergent code); `dep` makes the stamp wait for a loaded value
+#define PROBE_W(slot, dep)                                                                               \
+    do {                                                                                                 \
+        asm volatile("" ::"r"(dep) : "memory");                                                          \
+        const unsigned am_ = __activemask();                                                             \
+        if ((am_ & (0u - am_)) == (1u << (threadIdx.x & 31))) /* lowest lane that got here */            \
+            atomicMax(&cbtm::g_probe[cbtm::probe_frame() & (PROBE_FRAMES - 1)][slot], cbtm::probe_now()); \
+    } while (0)
 #define PROBE_SET_FRAME(f) do { if (threadIdx.x == 0) cbtm::probe_frame() = (f); __syncthreads(); } while (0)
 #define PROBE_T0(slot, f)                                                                                \
     do {                                                                                                 \
@@ -86,6 +94,7 @@ __device__ __forceinline__ unsigned long long probe_now()
 #else
 #define WORK_END(ctl, k) do { } while (0)
 #define PROBE(slot) do { } while (0)
+#define PROBE_W(slot, dep) do { } while (0)
 #define PROBE_SET_FRAME(f) do { } while (0)
 #define PROBE_T0(slot, f) do { } while (0)
 #endif
@@ -386,6 +395,26 @@ __device__ __forceinline__ void build_window_table(const FrameArgs &a, long long
 }
 
 // ---------------------------------------------------------------------------
+// What a thread learns about ITS rank of the CTA's first chunk (chunk == bid: the only chunk of a CTA
+// up to 75 k live bisectors) in one phase and needs again in a later one, kept in shared memory across
+// the grid barriers of the persistent kernel instead of being fetched again: the slot and the record
+// (P2), the final command word, the twin, the allocation count and the agreement reference (P3), the
+// reserved slots (P4).  Every value is private to the thread's rank or unchanged until the apply phase
+// writes (own records of consumed bisectors are never rewritten), so the copies cannot go stale.  It
+// removes the rank -> slot round trip from the head of P3 and both the rank-indexed and the own-record
+// round trips from the head of P5.  Lives in the index phase's staging area (dead between P1 and P6).
+// ---------------------------------------------------------------------------
+struct Carry {
+    int32_t s[CHUNK];
+    uint32_t id_lo[CHUNK], id_hi[CHUNK];
+    int32_t nx[CHUNK], pv[CHUNK], tw[CHUNK], j4[CHUNK];
+    uint32_t cmd[CHUNK];
+    int32_t mref[CHUNK];
+    uint32_t na[CHUNK];
+    int32_t res[4][CHUNK];
+};
+
+// ---------------------------------------------------------------------------
 // P2 = stage 4: evaluate verdicts and compute each rank's reservation need
 // (3d+4 for a split, 2 for a valid merge, 0 otherwise).  Splits walk their
 // compatibility chain OR-ing edge-split bits (kernels.py:289-310); merges OR
@@ -430,7 +459,7 @@ __device__ __forceinline__ void walk_split_chain(const cbtm_pool &p, int32_t s)
 }
 
 __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb,
-                                               const double *prm_row = nullptr)
+                                               const double *prm_row = nullptr, Carry *carry = nullptr)
 {
     __shared__ double prm[CBTM_PRM_WORDS];
     __shared__ uint32_t wsum[CHUNK / 32], wmin[CHUNK / 32];
@@ -523,6 +552,14 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
             }
             a.ws.need8[i] = (uint8_t)need;
             a.ws.mbits8[i] = (uint8_t)mbits;
+            if (carry && chunk == bid) { // (here, not at the loads: a store in between would serialise them)
+                carry->s[tid] = s;
+                carry->id_lo[tid] = (uint32_t)id;
+                carry->id_hi[tid] = (uint32_t)(id >> 32);
+                carry->nx[tid] = gathered.nx;
+                carry->pv[tid] = gathered.pv;
+                carry->j4[tid] = (mbits & CBTM_CMD_QUAD) ? j4 : -1;
+            }
         }
         PROBE(9); // classify: verdicts and needs known
 #ifdef CBTM_DEBUG_TIMING
@@ -801,7 +838,8 @@ __device__ __forceinline__ void phase_scatter(const FrameArgs &a, uint32_t bid, 
 // live slot (merge_ref: owner and pair of every agreed-merge member) and count
 // each rank's allocations (kernels.py:347-368).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb)
+__device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb,
+                                            Carry *carry = nullptr)
 {
     __shared__ uint32_t wsum[CHUNK / 32];
     __shared__ uint32_t acc[4];
@@ -817,12 +855,15 @@ __device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t n, uint
         const uint32_t i = chunk * CHUNK + tid;
         uint32_t na = 0;
         if (i < n) {
-            const int32_t s = p.cache_live[i];
-            const int32_t j4_hint = a.ws.j4s[i]; // meaningful only under a QUAD command of this frame
+            const bool carried = carry && chunk == bid; // CTA-uniform
+            const int32_t s = carried ? carry->s[tid] : p.cache_live[i];
+            const int32_t j4_hint = carried ? carry->j4[tid] : a.ws.j4s[i]; // meaningful only under a QUAD command of this frame
             // the record's fields together with its command word: one round trip instead of two
+            // (carried: the command word alone, and the twin for the apply phase)
             const uint32_t cmd = p.commands[s];
-            const uint64_t js = p.ids[s];
-            const int32_t nx = p.nexts[s], pv = p.prevs[s];
+            const uint64_t js = carried ? ((uint64_t)carry->id_hi[tid] << 32) | carry->id_lo[tid] : p.ids[s];
+            const int32_t nx = carried ? carry->nx[tid] : p.nexts[s], pv = carried ? carry->pv[tid] : p.prevs[s];
+            const int32_t tw = carried ? p.twins[s] : -1;
             const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
             int32_t ref = -1;
             if (sm) {
@@ -857,6 +898,12 @@ __device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t n, uint
             }
             a.ws.merge_ref[s] = ref;
             a.ws.nalloc8[i] = (uint8_t)na;
+            if (carried) {
+                carry->cmd[tid] = cmd;
+                carry->mref[tid] = ref;
+                carry->na[tid] = na;
+                carry->tw[tid] = tw;
+            }
         }
         const uint32_t sum = warp_sum(na);
         if (lane == 0) wsum[warp] = sum;
@@ -914,7 +961,8 @@ __device__ __forceinline__ uint64_t cta_range_sum(const uint32_t *v, uint32_t lo
 // then just picks its slots; outside the table (fragmented pool) each thread
 // descends the tree.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb)
+__device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb,
+                                              Carry *carry = nullptr)
 {
     __shared__ uint32_t scratch[32];
     __shared__ unsigned long long scratch64[CHUNK / 32];
@@ -940,8 +988,9 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, ui
         // chunks between the previous chunk of this CTA and this one
         const uint32_t total = a.ws.chunk_alloc[chunk];
         const uint32_t i = chunk * CHUNK + tid;
-        const uint32_t na = i < n ? a.ws.nalloc8[i] : 0;
-        const int32_t s = i < n ? p.cache_live[i] : -1;
+        const bool carried = carry && chunk == bid; // CTA-uniform
+        const uint32_t na = i < n ? (carried ? carry->na[tid] : a.ws.nalloc8[i]) : 0;
+        const int32_t s = i < n ? (carried ? carry->s[tid] : p.cache_live[i]) : -1;
         off += (long long)cta_range_sum(a.ws.chunk_alloc, summed, chunk, scratch64);
         summed = chunk;
         if (total == 0) continue; // CTA-uniform
@@ -1021,6 +1070,7 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, ui
                     p.cache_free[r] = slot;
                 }
                 p.reserved[4 * (size_t)s + k] = slot;
+                if (carried) carry->res[k][tid] = slot;
             }
         }
         __syncthreads(); // slots / s_j0 are reused by the next chunk
@@ -1225,10 +1275,56 @@ __device__ __forceinline__ void set_live(const BitSink &b, int32_t slot)
     b.dirty[(uint32_t)slot >> LEAF_LOG2] = 1;
 }
 
-__device__ __forceinline__ void set_free(const BitSink &b, int32_t slot)
+// Stage 8 for a whole warp at once.  The slots a warp flips are neighbours -- consecutive ranks free
+// consecutive live slots and reserve consecutive free ranks -- so its lanes hit a handful of 32-bit words
+// of the bitfield and ONE byte of the dirty map; sent one by one, a frame's ~50 k atomics and as many
+// mark stores queue up on a few L2 sectors (same-address requests are served one per clock by their
+// slice) and their drain is the tail of the apply phase.  Here a lane hands in one (word, mask) pair;
+// runs of lanes with the same word (the active list is sorted by slot, so equal words sit in
+// neighbouring lanes) are OR-ed together with five shuffle steps and the first lane of each run issues
+// ONE atomic and ONE mark.  Correct for any arrangement of the words: a lane is skipped only if the lane
+// before it carries the same word, and then that run's leader has collected its bits; OR / AND-NOT are
+// idempotent, so bits that two leaders both collected do no harm.  word = ~0u: nothing to flip.
+// All 32 lanes must call it.
+__device__ __forceinline__ void warp_flip(const BitSink &b, uint32_t word, uint32_t mask, bool live, int lane)
 {
-    atomicAnd(&b.bits32[slot >> 5], ~(1u << (slot & 31)));
-    b.dirty[(uint32_t)slot >> LEAF_LOG2] = 1;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t w2 = __shfl_down_sync(FULL_MASK, word, d);
+        const uint32_t m2 = __shfl_down_sync(FULL_MASK, mask, d);
+        if (lane + d < 32 && w2 == word) mask |= m2;
+    }
+    const uint32_t before = __shfl_up_sync(FULL_MASK, word, 1);
+    if (word != ~0u && (lane == 0 || before != word)) {
+        if (live) atomicOr(&b.bits32[word], mask);
+        else atomicAnd(&b.bits32[word], ~mask);
+        b.dirty[word >> (LEAF_LOG2 - 5)] = 1;
+    }
+}
+
+// the slot a bisector frees and the first `na` of the slots it reserved (all lanes of the warp call it;
+// freed < 0: nothing freed)
+__device__ __forceinline__ void warp_flip_bits(const BitSink &b, int32_t freed, uint32_t na, int4 res, int lane)
+{
+    warp_flip(b, freed >= 0 ? (uint32_t)freed >> 5 : ~0u, freed >= 0 ? 1u << (freed & 31) : 0u, false, lane);
+    // the 2..4 reserved slots are consecutive free ranks: almost always one word, sometimes two; whatever
+    // does not share the first slot's word goes out on its own
+    int32_t slot[4] = {na > 0 ? res.x : -1, na > 1 ? res.y : -1, na > 2 ? res.z : -1, na > 3 ? res.w : -1};
+    uint32_t word = ~0u, mask = 0;
+    if (slot[0] >= 0) {
+        word = (uint32_t)slot[0] >> 5;
+        mask = 1u << (slot[0] & 31);
+#pragma unroll
+        for (int k = 1; k < 4; ++k)
+            if (slot[k] >= 0 && ((uint32_t)slot[k] >> 5) == word) {
+                mask |= 1u << (slot[k] & 31);
+                slot[k] = -1;
+            }
+    }
+    warp_flip(b, word, mask, true, lane);
+#pragma unroll
+    for (int k = 1; k < 4; ++k)
+        if (slot[k] >= 0) set_live(b, slot[k]);
 }
 
 // kernels.py:373-461 restated over the two halves of the bisector
@@ -1250,18 +1346,16 @@ __device__ __forceinline__ OwnRecord load_own(const cbtm_pool &p, int32_t s)
     return r;
 }
 
-__device__ __forceinline__ void apply_split(ApplyCtx &cx, int32_t s, uint32_t sm, const OwnRecord &own)
+// tn / tp / tt: the resolved bundles of the neighbours across the next, prev and twin edge (phase_apply
+// fetches them: bundles, then the parents of those that merge away; only then is anything consumed or
+// stored -- a store in between would serialise the loads)
+__device__ __forceinline__ void apply_split(ApplyCtx &cx, int32_t s, uint32_t sm, const OwnRecord &own,
+                                            const Neighbour &tn, const Neighbour &tp, const Neighbour &tt)
 {
     const cbtm_pool &p = cx.p;
     const uint64_t j = own.id;
-    const int32_t nb_n = own.nx, nb_p = own.pv, nb_t = own.tw;
+    const int32_t nb_n = own.nx, nb_p = own.pv;
     const int4 r4 = own.res;
-    // round trip: the three neighbour bundles; round trip: the parents of those that merge away;
-    // only then is anything consumed or stored (a store in between would serialise the loads)
-    Neighbour tn = load_neighbour(cx, nb_n), tp = load_neighbour(cx, nb_p), tt = load_neighbour(cx, nb_t);
-    resolve_parent(cx, tn);
-    resolve_parent(cx, tp);
-    resolve_parent(cx, tt);
     const bool split_p = sm & CBTM_CMD_SPLIT_P, split_n = sm & CBTM_CMD_SPLIT_N;
     const int left_n = split_p ? 2 : 1;
     const int32_t left_last = split_p ? r4.y : r4.x;
@@ -1313,13 +1407,9 @@ __device__ __forceinline__ void apply_split(ApplyCtx &cx, int32_t s, uint32_t sm
     if (!split_n && nb_n >= 0 && survives(tn)) redirect_to(p, tn, s, right_first, E_PREV);
     if (!split_p && nb_p >= 0 && survives(tp)) redirect_to(p, tp, s, r4.x, E_NEXT);
 
-    // stage 8
-    const BitSink bits32{reinterpret_cast<uint32_t *>(p.bits), cx.dirty};
-    set_free(bits32, s);
-    set_live(bits32, r4.x);
-    set_live(bits32, r4.y);
-    if (left_n + (split_n ? 2 : 1) > 2) set_live(bits32, r4.z);
-    if (split_p && split_n) set_live(bits32, r4.w);
+    // (stage 8: phase_apply flipped the bits of this bisector's slot and of its reservation up front)
+    (void)left_n;
+    PROBE_W(25, 0); // apply: split stores issued
 }
 
 // one sibling pair (even id e, odd id o) collapses into parent slot par; n_ext / q_ext are the
@@ -1338,7 +1428,12 @@ __device__ __forceinline__ void apply_merged_pair(ApplyCtx &cx, int32_t e, int32
     if (q_ext.slot >= 0 && survives(q_ext)) redirect_to(p, q_ext, e, par, E_NEXT);
 }
 
-__device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb)
+// (Dealing the 32-rank groups of the active list round-robin to the warps of the grid was measured too: the
+// bisectors a frame consumes are not spread evenly over the ranks -- 38 .. 93 per chunk on average, 256 in
+// the fullest chunks of the Earth sweep, benchmarks/apply_imbalance.py -- but a balanced deal gives up the
+// carried values, and the two round trips that costs outweigh the balance: 5.4 vs 4.9 us.)
+__device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb,
+                                            Carry *carry = nullptr)
 {
     __shared__ uint32_t poisoned;
     const cbtm_pool &p = a.pool;
@@ -1351,65 +1446,99 @@ __device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t n, uint
 
     for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
         const uint32_t i = chunk * CHUNK + tid;
-        if (i >= n) continue;
+        const bool valid = i < n;
         // round trip 1: by rank; round trip 2: everything about the own record at once
-        const uint32_t na = a.ws.nalloc8[i];
-        const int32_t s = p.cache_live[i];
-        const int32_t j4_hint = a.ws.j4s[i];
-        const uint32_t cmd = p.commands[s];
-        const int32_t mref = a.ws.merge_ref[s];
+        // (carried: neither -- the thread has all of it from the earlier phases of this frame)
+        const bool carried = carry && chunk == bid; // CTA-uniform
+        uint32_t na = 0, cmd = 0;
+        int32_t s = -1, j4_hint = -1, mref = -1;
         OwnRecord own = {};
-        if (na) own = load_own(p, s);
-        const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
-        if (na == 0) {
-            // not allocating: either untouched, or a non-owner member of an agreed merge
-            if (!sm && mref >= 0) set_free(bits32, s);
-            continue;
+        if (valid) {
+            na = carried ? carry->na[tid] : a.ws.nalloc8[i];
+            s = carried ? carry->s[tid] : p.cache_live[i];
+            j4_hint = carried ? carry->j4[tid] : a.ws.j4s[i];
+            cmd = carried ? carry->cmd[tid] : p.commands[s];
+            mref = carried ? carry->mref[tid] : a.ws.merge_ref[s];
+            if (na && carried) {
+                own.id = ((uint64_t)carry->id_hi[tid] << 32) | carry->id_lo[tid];
+                own.nx = carry->nx[tid];
+                own.pv = carry->pv[tid];
+                own.tw = carry->tw[tid];
+                own.res = make_int4(carry->res[0][tid], carry->res[1][tid], carry->res[2][tid], carry->res[3][tid]);
+            } else if (na) {
+                own = load_own(p, s);
+            }
         }
-        if (sm) {
-            apply_split(cx, s, sm, own);
-        } else { // owner of an agreed merge: kernels.py:464-491, 562-594, 624-628
-            set_free(bits32, s);
-            const uint64_t js = own.id;
-            const MergeCfg c = merge_config_admitted(js, own.nx, own.pv, cmd, j4_hint);
-            const bool quad = c.kind == 2;
-            // round trip: ids and twin pointers of the other members (parities are not known yet, so
-            // everything that may be needed is fetched); round trip: the four outer neighbours'
-            // bundles; round trip: their parents if they merge away; then the stores
-            const uint64_t id_sib = p.ids[c.sib];
-            const int32_t tw_sib = p.twins[c.sib];
-            uint64_t jo = 0, id_j4 = 0;
-            int32_t tw_oth = -1, tw_j4 = -1;
-            if (quad) {
+        const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
+        // stage 8 first, by the whole warp (kernels.py:598-632): a bisector that splits or belongs to an
+        // agreed merge frees its slot, the first na reserved slots come alive
+        warp_flip_bits(bits32, (valid && (sm || mref >= 0)) ? s : -1, na, own.res, tid & 31);
+        if (na == 0) continue; // not allocating: untouched, or a non-owner member of an agreed merge
+        // A warp holds splitting bisectors and owners of agreed merges side by side, and the two kinds
+        // need different things: the split's three neighbour bundles and their parents; the merge's other
+        // members first (kernels.py:464-491, 562-594, 624-628), then the bundles of the pairs' outer
+        // neighbours and their parents.  Written as two branches the warp would run one chain of round
+        // trips after the other; here the loads of both kinds are issued level by level -- the split's
+        // bundles go out while the merge's members are on their way, the bundles of both kinds land in
+        // the same four variables, and the parents are resolved by common code -- so the phase is three
+        // round trips long, not five.
+        const bool is_split = sm != 0;
+        MergeCfg c = {0, -1, -1, -1, 0, 0, 0};
+        uint64_t id_sib = 0, jo = 0, id_j4 = 0;
+        int32_t tw_sib = -1, tw_oth = -1, tw_j4 = -1;
+        if (!is_split) { // level 1 of a merge: ids and twin pointers of the other members (parities are not
+                         // known yet, so everything that may be needed is fetched)
+            c = merge_config_admitted(own.id, own.nx, own.pv, cmd, j4_hint);
+            id_sib = p.ids[c.sib];
+            tw_sib = p.twins[c.sib];
+            if (c.kind == 2) {
                 jo = p.ids[c.oth];
                 id_j4 = p.ids[c.j4];
                 tw_oth = p.twins[c.oth];
                 tw_j4 = p.twins[c.j4];
             }
-            const bool s_even = !(js & 1), oth_even = !(jo & 1);
+        }
+        Neighbour b0, b1, b2, b3; // split: across next, prev, twin, (none); merge: n1, q1, n2, q2
+        const bool quad = c.kind == 2;
+        const uint64_t js = own.id;
+        const bool s_even = !(js & 1);
+        if (is_split) { // level 1 of a split
+            b0 = load_neighbour(cx, own.nx);
+            b1 = load_neighbour(cx, own.pv);
+            b2 = load_neighbour(cx, own.tw);
+            b3 = load_neighbour(cx, -1);
+        }
+        bool oth_even = false;
+        if (!is_split) { // level 2 of a merge (the members have arrived)
+            PROBE_W(21, (uint32_t)id_sib ^ (uint32_t)tw_sib ^ (uint32_t)jo ^ (uint32_t)id_j4 ^ (uint32_t)tw_oth ^ (uint32_t)tw_j4); // apply: merge members arrived
+            oth_even = !(jo & 1);
+            b0 = load_neighbour(cx, s_even ? tw_sib : own.tw); // across twins[o1]
+            b1 = load_neighbour(cx, s_even ? own.tw : tw_sib); // across twins[e1]
+            b2 = load_neighbour(cx, quad ? (oth_even ? tw_j4 : tw_oth) : -1);
+            b3 = load_neighbour(cx, quad ? (oth_even ? tw_oth : tw_j4) : -1);
+        }
+        PROBE_W(18, b0.cmd ^ b1.cmd ^ b2.cmd ^ b3.cmd ^ (uint32_t)(b0.res.x ^ b1.res.x ^ b2.res.x ^ b3.res.x ^ b0.mref ^ b1.mref ^ b2.mref ^ b3.mref)); // apply: neighbour bundles arrived
+        resolve_parent(cx, b0);
+        resolve_parent(cx, b1);
+        resolve_parent(cx, b2);
+        resolve_parent(cx, b3);
+        PROBE_W(19, b0.parent ^ b1.parent ^ b2.parent ^ b3.parent); // apply: parents arrived (first store follows)
+        if (is_split) {
+            apply_split(cx, s, sm, own, b0, b1, b2);
+        } else {
             const int32_t e1 = s_even ? s : c.sib, o1 = s_even ? c.sib : s;
             const int32_t e2 = oth_even ? c.oth : c.j4, o2 = oth_even ? c.j4 : c.oth;
-            Neighbour n1 = load_neighbour(cx, s_even ? tw_sib : own.tw); // across twins[o1]
-            Neighbour q1 = load_neighbour(cx, s_even ? own.tw : tw_sib); // across twins[e1]
-            Neighbour n2 = load_neighbour(cx, quad ? (oth_even ? tw_j4 : tw_oth) : -1);
-            Neighbour q2 = load_neighbour(cx, quad ? (oth_even ? tw_oth : tw_j4) : -1);
-            resolve_parent(cx, n1);
-            resolve_parent(cx, q1);
-            resolve_parent(cx, n2);
-            resolve_parent(cx, q2);
             const int32_t p1 = own.res.x;
             const uint64_t id_e1 = s_even ? js : id_sib;
             if (quad) {
                 const int32_t p2 = own.res.y;
                 const uint64_t id_e2 = oth_even ? jo : id_j4;
-                apply_merged_pair(cx, e1, o1, id_e1, p1, p2, n1, q1);
-                apply_merged_pair(cx, e2, o2, id_e2, p2, p1, n2, q2);
-                set_live(bits32, p1);
-                set_live(bits32, p2);
+                apply_merged_pair(cx, e1, o1, id_e1, p1, p2, b0, b1);
+                apply_merged_pair(cx, e2, o2, id_e2, p2, p1, b2, b3);
             } else {
-                apply_merged_pair(cx, e1, o1, id_e1, p1, -1, n1, q1);
-                set_live(bits32, p1);
+                apply_merged_pair(cx, e1, o1, id_e1, p1, -1, b0, b1);
             }
+            PROBE_W(26, 0); // apply: merge stores issued
         }
     }
     // (the frame's counters were taken in phase_agree; what is left to report is the poison count)
@@ -1474,7 +1603,8 @@ __global__ void __launch_bounds__(CHUNK) k_publish(const __grid_constant__ Frame
 // ---------------------------------------------------------------------------
 // the persistent frame kernel: n_frames full updates in one cooperative launch
 // ---------------------------------------------------------------------------
-constexpr int FRAMES_DYN_SMEM = IDX_WARPS * IDX_STAGE_WORDS * 4; // 36 KB: index staging
+constexpr int FRAMES_DYN_SMEM = IDX_WARPS * IDX_STAGE_WORDS * 4; // 36 KB: index staging (P1), Carry (P2-P5), tile values (P6)
+static_assert(sizeof(Carry) <= FRAMES_DYN_SMEM, "the carry lives in the index staging area");
 
 // CTAS = co-resident CTAs per SM the register budget is cut for: 2 (latency-bound frames of a few hundred
 // chunks: fewer CTAs, cheaper barriers, no spills) or 4 (CBTM_POOL_WIDE_GRID, pools with 10^5 .. 10^7 live
@@ -1517,7 +1647,8 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         if (stamp) stamp[1] = global_ns();
         const uint32_t n = p.counters[1];      // the frame's live count: one read per CTA, kept in a register
         const bool fast = fits_a_priori(p, n); // grid-uniform
-        phase_classify(a, n, bid, nb, (mailbox && f > 0) ? ctl->mb_prm : nullptr);
+        Carry *carry = reinterpret_cast<Carry *>(dyn_smem); // (the staging area of the index phase is free until P6)
+        phase_classify(a, n, bid, nb, (mailbox && f > 0) ? ctl->mb_prm : nullptr, carry);
         WORK_END(ctl, 1);
         grid.sync();
         const bool fits = fast || frame_fits(a, n); // grid-uniform
@@ -1540,7 +1671,7 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
             build_window_table(a, ctl->T);
             PROBE(12); // window table built
         }
-        phase_agree(a, n, bid, nb);
+        phase_agree(a, n, bid, nb, carry);
         PROBE(13); // agreement done
         WORK_END(ctl, 2);
         grid.sync();
@@ -1554,13 +1685,13 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         // fewest chunks does it (none at all for up to 75 k live bisectors).
         if (bid == nb - 1 && !mailbox && f == n_frames - 1 && p.stats)
             publish_early(ctl->stats, p.stats, ctl->phase_t[f & 1], threadIdx.x);
-        phase_reserve(a, n, bid, nb);
+        phase_reserve(a, n, bid, nb, carry);
         PROBE(17); // reserve done
         WORK_END(ctl, 3);
         grid.sync();
         if (stamp) stamp[4] = global_ns();
         PROBE_T0(4, f);
-        phase_apply(a, n, bid, nb);
+        phase_apply(a, n, bid, nb, carry);
         PROBE(20); // apply done
         WORK_END(ctl, 4);
         grid.sync();
