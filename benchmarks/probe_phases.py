@@ -34,14 +34,13 @@ L.cbtm_debug_probes(buf.ctypes.data, 1)
 t = buf[:K].astype(np.int64)
 names = {0: "frame start", 7: "  index: work done (latest CTA)", 1: "P2 start (classify)", 8: "  gathers issued", 9: "  verdicts + needs known",
          10: "  commands scattered", 2: "P3 start (agree)", 12: "  window table built (CTA nb-1)", 13: "  agreement done (latest CTA)",
-         3: "P4 start (reserve)", 14: "  prefix known", 15: "  window block found", 16: "  slots expanded", 17: "  reserve done",
-         4: "P5 start (apply)", 18: "  splits: neighbour bundles arrived (latest warp)", 19: "  splits: parents arrived", 25: "  splits: stores issued", 21: "  merges: members arrived", 23: "  merges: neighbour bundles arrived",
-         24: "  merges: parents arrived", 26: "  merges: stores issued", 20: "  apply done", 5: "P6 start (reduce)", 22: "  reduce done", 6: "frame end (after last barrier)"}
-order = [0, 7, 1, 8, 9, 10, 2, 12, 13, 3, 14, 15, 16, 17, 4, 18, 19, 25, 21, 23, 24, 26, 20, 5, 22, 6]
+         3: "P4 start (reserve)", 14: "  prefix known", 15: "  window block found", 27: "  first block's bits arrived (latest warp)", 28: "  blocks expanded (latest warp)", 16: "  slots expanded", 17: "  reserve done",
+         4: "P5 start (apply)", 18: "  neighbour bundles arrived (splits and merges, latest warp)", 19: "  parents arrived", 25: "  splits: stores issued", 21: "  merges: members arrived", 26: "  merges: stores issued", 20: "  apply done", 5: "P6 start (reduce)", 22: "  reduce done", 6: "frame end (after last barrier)"}
+order = [0, 7, 1, 8, 9, 10, 2, 12, 13, 3, 14, 15, 27, 28, 16, 17, 4, 21, 18, 19, 25, 26, 20, 5, 22, 6]
 print(f"2^{depth} pool, {K} frames, live {np.mean([r.live_before for r in rows]):.0f}: us since frame start (mean over frames)")
 prev = None
 for k in order:
     ok = t[:, k] > 0
     rel = (t[ok, k] - t[ok, 0]) / 1e3
-    print(f"{names[k]:52s} {rel.mean():7.2f}" + (f"   (+{rel.mean() - prev:5.2f})" if prev is not None else ""))
+    print(f"{names[k]:62s} {rel.mean():7.2f}" + (f"   (+{rel.mean() - prev:5.2f})" if prev is not None else ""))
     prev = rel.mean()

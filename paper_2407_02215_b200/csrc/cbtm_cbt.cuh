@@ -843,10 +843,11 @@ __device__ __forceinline__ void index_phase(const uint32_t *bits32, const uint32
                     if (word == 0u) continue;
                     const uint32_t r1 = __popc(word & lane_lt);
                     const int32_t slot = base + w * 32 + lane;
-                    if ((word >> lane) & 1u) {
-                        st[p1 + r1] = slot;
-                        if (RESET) reset_cmds[slot] = 0u; // stage 3 (kernels.py:256-259)
-                    }
+                    // (two predicated stores: one `if` around both made the compiler emit a divergent
+                    // branch with a reconvergence barrier per word)
+                    const bool bit = (word >> lane) & 1u;
+                    if (bit) st[p1 + r1] = slot;
+                    if (RESET && bit) reset_cmds[slot] = 0u; // stage 3 (kernels.py:256-259)
                     p1 += __popc(word);
                 }
             } else { // tiny pool: a single partial block

@@ -107,6 +107,7 @@ namespace cbtm {
 constexpr int TAIL_MAX = 96;
 constexpr int MAX_SEQ_FRAMES = 4096;
 constexpr int WIN_MAX = 4096;       // leaf blocks covered by the free-rank window table
+constexpr int WIN_SMEM = 1024;      // ... of which the reserve phase keeps up to this many in shared memory
 
 // device-resident control block of one pool (lives in the workspace)
 struct Control {
@@ -931,11 +932,16 @@ __device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t n, uint
         atomicAdd((unsigned long long *)&a.ws.ctl->stats[CBTM_STAT_SPLIT_FREED + tid], (unsigned long long)acc[tid]);
 }
 
-// sum of v[lo, hi) by the whole CTA (every thread gets it); scratch: CHUNK / 32 words
-__device__ __forceinline__ uint64_t cta_range_sum(const uint32_t *v, uint32_t lo, uint32_t hi, unsigned long long *scratch)
+// sum of v[lo, hi) by the whole CTA (every thread gets it); scratch: CHUNK / 32 words.
+// between_loads_and_barrier() runs once the loads have been issued and before the first CTA barrier (for
+// shared-memory stores that wait on loads of their own and want the barrier)
+template <typename F>
+__device__ __forceinline__ uint64_t cta_range_sum(const uint32_t *v, uint32_t lo, uint32_t hi, unsigned long long *scratch,
+                                                  F between_loads_and_barrier)
 {
     unsigned long long acc = 0;
     for (uint32_t j = lo + threadIdx.x; j < hi; j += CHUNK) acc += v[j];
+    between_loads_and_barrier();
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, o);
     if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = acc;
@@ -945,6 +951,11 @@ __device__ __forceinline__ uint64_t cta_range_sum(const uint32_t *v, uint32_t lo
     for (int w = 0; w < CHUNK / 32; ++w) total += scratch[w];
     __syncthreads();
     return total;
+}
+
+__device__ __forceinline__ uint64_t cta_range_sum(const uint32_t *v, uint32_t lo, uint32_t hi, unsigned long long *scratch)
+{
+    return cta_range_sum(v, lo, hi, scratch, [] {});
 }
 
 // ---------------------------------------------------------------------------
@@ -980,6 +991,21 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, ui
     WORK_END(ctl, 6); // (debug) latest CTA entering the phase = barrier exit skew
     const uint32_t win_n = ctl->win_n, win_lo = ctl->win_lo; // CTA-uniform: written before the last barrier
     const uint32_t win_first = win[0]; // (garbage while win_n == 0, never used then)
+    // The window table of a frame is short (one entry per leaf block the frame allocates from: a few
+    // dozen): it is copied into shared memory while the first chunk's prefix loads are in flight, so that
+    // finding the chunk's window block afterwards is not another round trip to L2.
+    __shared__ uint32_t s_win[WIN_SMEM + 1];
+    const bool win_cached = win_n != 0 && win_n <= (uint32_t)WIN_SMEM; // CTA-uniform
+    uint32_t wreg[WIN_SMEM / CHUNK + 1];
+    if (win_cached) {
+#pragma unroll
+        for (int k = 0; k <= WIN_SMEM / CHUNK; ++k) {
+            const uint32_t j = (uint32_t)k * CHUNK + tid;
+            wreg[k] = j <= win_n ? win[j] : 0u;
+        }
+    }
+    bool win_pending = win_cached;
+    const uint32_t *wtab = win_cached ? s_win : win;
 
     long long off = 0;      // slots allocated by chunks [0, summed)
     uint32_t summed = 0;
@@ -991,7 +1017,16 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, ui
         const bool carried = carry && chunk == bid; // CTA-uniform
         const uint32_t na = i < n ? (carried ? carry->na[tid] : a.ws.nalloc8[i]) : 0;
         const int32_t s = i < n ? (carried ? carry->s[tid] : p.cache_live[i]) : -1;
-        off += (long long)cta_range_sum(a.ws.chunk_alloc, summed, chunk, scratch64);
+        off += (long long)cta_range_sum(a.ws.chunk_alloc, summed, chunk, scratch64, [&] {
+            if (win_pending) { // (first chunk: the table lands next to the prefix; the barriers of the sum publish it)
+#pragma unroll
+                for (int k = 0; k <= WIN_SMEM / CHUNK; ++k) {
+                    const uint32_t j = (uint32_t)k * CHUNK + tid;
+                    if (j <= win_n) s_win[j] = wreg[k];
+                }
+            }
+        });
+        win_pending = false;
         summed = chunk;
         if (total == 0) continue; // CTA-uniform
         PROBE(14); // reserve: prefix known
@@ -1008,7 +1043,7 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, ui
                 bool hit = false;
                 if ((uint32_t)tid < top) {
                     const uint32_t j = top - 1 - tid;
-                    if (win[j] <= lo_rank && lo_rank < win[j + 1]) {
+                    if (wtab[j] <= lo_rank && lo_rank < wtab[j + 1]) {
                         s_j0 = j;
                         hit = true;
                     }
@@ -1028,12 +1063,16 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, ui
                 first = 0xffffffffu; // beyond the table: ends the loop
                 word = 0;
                 if (j < win_n) {
-                    first = win[j]; // free rank of the block's first free slot
-                    word = valid ? bits32[(size_t)(win_lo + j) * 32 + lane] : 0xffffffffu;
+                    first = wtab[j]; // free rank of the block's first free slot
+                    // (with the table in shared memory `first` is known at once: a block beyond the chunk's
+                    // interval is not fetched -- its line would come from DRAM and the warp would wait for it)
+                    if (!win_cached || first < hi_rank)
+                        word = valid ? bits32[(size_t)(win_lo + j) * 32 + lane] : 0xffffffffu;
                 }
             };
             uint32_t first, word, first_nx, word_nx;
             fetch(s_j0 + warp, first, word);
+            PROBE_W(27, word ^ first); // reserve: first block's bits arrived
             for (uint32_t j = s_j0 + warp; first < hi_rank; j += CHUNK / 32) {
                 fetch(j + CHUNK / 32, first_nx, word_nx);
                 const uint32_t b = win_lo + j;
@@ -1042,19 +1081,25 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, ui
                 uint32_t r = first + warp_inclusive_scan(c) - c; // free rank of this lane's first free slot
                 const int32_t lane_base = (int32_t)(b * g.span + lane * 32);
                 if (r + c > lo_rank && r < hi_rank) { // some of this word's free slots are wanted
-                    // bit by bit with plain ALU operations (find-first-set sits on the quarter-rate
-                    // unit and made this loop the longest step of the phase)
+                    // Bit by bit, BRANCH FREE: the position in the interval is an unsigned counter that is in
+                    // range iff it is below the interval's length (ranks before the interval wrap around),
+                    // a step is test-bit / compare / predicated store / add.  (Written with the store and
+                    // the increment inside `if (bit)` the compiler emitted a divergent branch with a
+                    // reconvergence barrier per step: 32 of them, ~2 us per leaf block and the longest
+                    // step of the phase.)
+                    uint32_t at = r - lo_rank;
+                    const uint32_t len = hi_rank - lo_rank;
 #pragma unroll
                     for (int k = 0; k < 32; ++k) {
-                        if ((z >> k) & 1u) {
-                            if (r >= lo_rank && r < hi_rank) slots[r - lo_rank] = lane_base + k;
-                            ++r;
-                        }
+                        const uint32_t bit = (z >> k) & 1u;
+                        if (bit != 0u && at < len) slots[at] = lane_base + k;
+                        at += bit;
                     }
                 }
                 first = first_nx;
                 word = word_nx;
             }
+            PROBE_W(28, first); // reserve: this warp's blocks expanded
             __syncthreads();
             WORK_END(ctl, 8); // slots expanded
             PROBE(16);
