@@ -311,9 +311,11 @@ k_classify(const __grid_constant__ FrameArgs a, int8_t *verdict_out)
 // A whole CTA descends the counter heap eight levels per step (the 256 descendants of a
 // node eight levels down are contiguous): two round trips for D = 26.
 // scratch: 32 words, out: 2 words of shared memory.
+// first_step: the counter this thread needs for the first step (node (1 << s0) + tid, s0 = min(lc, 8)),
+// fetched by the caller ahead of time -- it does not depend on the rank (nullptr: fetched here).
 __device__ __forceinline__ void cta_find_free_block(const uint32_t *counters, const Geo &g, uint32_t rank,
                                                     uint32_t *scratch, uint32_t *out, uint32_t &block,
-                                                    uint32_t &free_before)
+                                                    uint32_t &free_before, const uint32_t *first_step = nullptr)
 {
     const int tid = threadIdx.x;
     uint32_t idx = 0, before = 0;
@@ -322,7 +324,10 @@ __device__ __forceinline__ void cta_find_free_block(const uint32_t *counters, co
         const int s = g.lc - l < 8 ? g.lc - l : 8;
         const uint32_t fan = 1u << s;
         const uint32_t child_span = (uint32_t)(g.n >> (l + s));
-        const uint32_t z = (uint32_t)tid < fan ? child_span - counters[(1u << (l + s)) + (idx << s) + tid] : 0u;
+        const uint32_t ones = (uint32_t)tid < fan ? ((l == 0 && first_step) ? *first_step
+                                                                            : counters[(1u << (l + s)) + (idx << s) + tid])
+                                                  : 0u;
+        const uint32_t z = (uint32_t)tid < fan ? child_span - ones : 0u;
         uint32_t total;
         const uint32_t incl = block_inclusive_scan<CHUNK>(z, scratch, &total);
         if ((uint32_t)tid == fan - 1) { // default: the last child (rank beyond the free count)
@@ -352,7 +357,7 @@ __device__ __forceinline__ void cta_find_free_block(const uint32_t *counters, co
 // free rank T - 1.  A is not known yet when T is, so the table is anchored at
 // the top: it covers the last WIN_MAX leaf blocks up to that one;
 // win_prefix[j] = free slots before leaf block win_lo + j.  (One CTA.)
-__device__ __forceinline__ void build_window_table(const FrameArgs &a, long long T)
+__device__ __forceinline__ void build_window_table(const FrameArgs &a, long long T, const uint32_t *first_step = nullptr)
 {
     __shared__ uint32_t scratch[32];
     __shared__ uint32_t s_out[2];
@@ -363,7 +368,8 @@ __device__ __forceinline__ void build_window_table(const FrameArgs &a, long long
     if (tid == 0) ctl->win_n = 0;
     if (T <= 0 || (p.flags & (CBTM_POOL_FULL_FREE_CACHE | CBTM_POOL_DESCEND_FREE_RANKS))) return;
     uint32_t hi, before_hi;
-    cta_find_free_block(p.counters, g, (uint32_t)(T - 1), scratch, s_out, hi, before_hi);
+    cta_find_free_block(p.counters, g, (uint32_t)(T - 1), scratch, s_out, hi, before_hi, first_step);
+    const uint32_t ones_hi = p.counters[g.nblocks + hi]; // (issued with the loads below, not behind their scan)
     const uint32_t lo = hi + 1 > (uint32_t)WIN_MAX ? hi + 1 - WIN_MAX : 0u;
     const uint32_t nbw = hi - lo + 1;
     constexpr int PER = WIN_MAX / CHUNK;
@@ -379,7 +385,7 @@ __device__ __forceinline__ void build_window_table(const FrameArgs &a, long long
     uint32_t total;
     const uint32_t incl = block_inclusive_scan<CHUNK>(sum, scratch, &total);
     // free slots before block lo = (free before block hi) - (free in [lo, hi))
-    const uint32_t z_hi = g.span - p.counters[g.nblocks + hi];
+    const uint32_t z_hi = g.span - ones_hi;
     const uint32_t base = before_hi - (total - z_hi);
     uint32_t run = base + incl - sum;
 #pragma unroll
@@ -422,7 +428,9 @@ struct Carry {
 // their configuration bits (kernels.py:320-333).  OR is commutative, so the
 // final command words do not depend on scheduling.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void walk_split_chain(const cbtm_pool &p, int32_t s)
+// t0: twins[s] if the caller has it already (kNoTwinYet: fetched here)
+constexpr int32_t kNoTwinYet = INT32_MIN;
+__device__ __forceinline__ void walk_split_chain(const cbtm_pool &p, int32_t s, int32_t t0 = kNoTwinYet)
 {
     // Pointer fields do not change during this phase, so the twin's operators
     // are fetched while the atomic on `cur` is still in flight, and the twin's
@@ -432,7 +440,7 @@ __device__ __forceinline__ void walk_split_chain(const cbtm_pool &p, int32_t s)
     // chain", which only holds if nobody marks a node and then stops (a variant
     // that looked at the old value one hop late lost parts of chains).
     int32_t cur = s;
-    int32_t t = p.twins[cur];
+    int32_t t = t0 != kNoTwinYet ? t0 : p.twins[cur];
     for (int hops = 0;;) {
         int32_t t_twin = -1, t_next = -1, t_prev = -1;
         if (t >= 0) {
@@ -497,12 +505,15 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
         int32_t s = -1;
         struct {
             uint64_t id, js, jo;
-            int32_t sib, oth, j4, nx, pv;
-        } gathered = {0, 0, 0, -1, -1, -1, -1, -1};
+            int32_t sib, oth, j4, nx, pv, tw;
+        } gathered = {0, 0, 0, -1, -1, -1, -1, -1, -1};
         if (i < n) {
             s = p.cache_live[i];
             const uint64_t id = p.ids[s];
             const int32_t nx = p.nexts[s], pv = p.prevs[s];
+            // the twin rides along: a split's chain walk starts from it (one round trip less per walk)
+            // and the apply phase wants it (carried)
+            const int32_t tw = (fast || carry) ? p.twins[s] : kNoTwinYet;
             // what a merge request will ask about its sibling and the opposite pair: with the LOD
             // classifier gathered now, for everybody, so that the round trip hides behind the fp64 work;
             // the other verdict sources are known at once, so only merge requests gather (three scattered
@@ -517,7 +528,7 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
                 jo = p.ids[oth];
                 j4 = odd ? p.nexts[oth] : p.prevs[oth];
             }
-            gathered = {id, js, jo, sib, oth, j4, nx, pv};
+            gathered = {id, js, jo, sib, oth, j4, nx, pv, tw};
         }
         PROBE(8); // classify: gathers issued (loads may still be in flight)
         { // deepest live bisector of the frame
@@ -559,6 +570,7 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
                 carry->id_hi[tid] = (uint32_t)(id >> 32);
                 carry->nx[tid] = gathered.nx;
                 carry->pv[tid] = gathered.pv;
+                carry->tw[tid] = gathered.tw;
                 carry->j4[tid] = (mbits & CBTM_CMD_QUAD) ? j4 : -1;
             }
         }
@@ -572,7 +584,7 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
             if (need == 2)
                 atomicOr(&p.commands[s], mbits);
             else if (need)
-                walk_split_chain(p, s);
+                walk_split_chain(p, s, gathered.tw);
             PROBE(10); // classify: commands scattered
             continue;
         }
@@ -619,13 +631,16 @@ __device__ __forceinline__ bool frame_fits(const FrameArgs &a, uint32_t n)
 
 // One CTA, once per frame, after the scatter: if the frame fits, T = total need and the other
 // per-frame fields phase_admit would have set; in any case need_total returns to zero.
-__device__ __forceinline__ void frame_totals(const FrameArgs &a, uint32_t n, bool fits)
+// Returns T (thread 0 only).
+__device__ __forceinline__ long long frame_totals(const FrameArgs &a, uint32_t n, bool fits)
 {
     const cbtm_pool &p = a.pool;
     Control *ctl = a.ws.ctl;
+    long long T = 0;
     if (threadIdx.x == 0) {
         const unsigned long long total = ctl->need_total;
         ctl->need_total = 0;
+        T = fits ? (long long)total : ctl->T; // (pressure path: phase_admit set it)
         if (fits) {
             ctl->n = n;
             ctl->F = (int64_t)(((uint64_t)1 << p.depth) - n);
@@ -637,6 +652,24 @@ __device__ __forceinline__ void frame_totals(const FrameArgs &a, uint32_t n, boo
         }
     }
     __syncthreads(); // ctl->T is read right away by the same CTA (window table)
+    return T;
+}
+
+// frame_totals + build_window_table by one CTA with the round trips that do not depend on each other
+// taken together: the counters of the descent's first step are fetched while thread 0 reads the frame's
+// total, and T reaches the other threads through shared memory instead of through the control block.
+__device__ __forceinline__ void frame_totals_and_window(const FrameArgs &a, uint32_t n, bool fits)
+{
+    __shared__ long long s_T;
+    const cbtm_pool &p = a.pool;
+    const Geo g = make_geo(p.depth);
+    const int s0 = g.lc < 8 ? g.lc : 8;
+    uint32_t first_step = 0;
+    if (g.lc > 0 && threadIdx.x < (1u << s0)) first_step = p.counters[(1u << s0) + threadIdx.x];
+    const long long T = frame_totals(a, n, fits);
+    if (threadIdx.x == 0) s_T = T;
+    __syncthreads();
+    build_window_table(a, s_T, g.lc > 0 ? &first_step : nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -860,11 +893,10 @@ __device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t n, uint
             const int32_t s = carried ? carry->s[tid] : p.cache_live[i];
             const int32_t j4_hint = carried ? carry->j4[tid] : a.ws.j4s[i]; // meaningful only under a QUAD command of this frame
             // the record's fields together with its command word: one round trip instead of two
-            // (carried: the command word alone, and the twin for the apply phase)
+            // (carried: the command word alone)
             const uint32_t cmd = p.commands[s];
             const uint64_t js = carried ? ((uint64_t)carry->id_hi[tid] << 32) | carry->id_lo[tid] : p.ids[s];
             const int32_t nx = carried ? carry->nx[tid] : p.nexts[s], pv = carried ? carry->pv[tid] : p.prevs[s];
-            const int32_t tw = carried ? p.twins[s] : -1;
             const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
             int32_t ref = -1;
             if (sm) {
@@ -903,7 +935,6 @@ __device__ __forceinline__ void phase_agree(const FrameArgs &a, uint32_t n, uint
                 carry->cmd[tid] = cmd;
                 carry->mref[tid] = ref;
                 carry->na[tid] = na;
-                carry->tw[tid] = tw;
             }
         }
         const uint32_t sum = warp_sum(na);
@@ -1623,8 +1654,7 @@ __global__ void __launch_bounds__(CHUNK) k_agree(const __grid_constant__ FrameAr
     // n from the CBT root: ctl->n is only written below (fast path) / by k_admit (slow path)
     const uint32_t n = a.pool.counters[1];
     if (blockIdx.x == gridDim.x - 1) {
-        frame_totals(a, n, fits_a_priori(a.pool, n) || frame_fits(a, n));
-        build_window_table(a, a.ws.ctl->T);
+        frame_totals_and_window(a, n, fits_a_priori(a.pool, n) || frame_fits(a, n));
     }
     phase_agree(a, n, blockIdx.x, gridDim.x);
 }
@@ -1712,8 +1742,7 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         // T is final: the free-rank window table is built by the CTA with the fewest chunks while the
         // others take the agreement snapshot (it was the straggler of P2 when built there)
         if (bid == nb - 1) {
-            frame_totals(a, n, fits);
-            build_window_table(a, ctl->T);
+            frame_totals_and_window(a, n, fits);
             PROBE(12); // window table built
         }
         phase_agree(a, n, bid, nb, carry);
@@ -1891,8 +1920,7 @@ k_frames_batch(const __grid_constant__ BatchArgs b, int n_pools, int n_frames)
         for (int q = 0; q < n_pools; ++q) {
             const uint32_t nq = b.a[q].pool.counters[1];
             if (vbid(q) == nb - 1) {
-                frame_totals(b.a[q], nq, (fits_mask >> q) & 1u);
-                build_window_table(b.a[q], b.a[q].ws.ctl->T);
+                frame_totals_and_window(b.a[q], nq, (fits_mask >> q) & 1u);
             }
             phase_agree(b.a[q], nq, vbid(q), nb);
             __syncthreads();
