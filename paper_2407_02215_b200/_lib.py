@@ -14,7 +14,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcbtm.so")
+# (CBTM_LIB: another build of the same library -- a debug build with timing probes, an older build for an
+# A/B measurement; still the CUDA library, there is no other implementation to fall back to)
+LIB_PATH = os.environ.get("CBTM_LIB") or os.path.join(_HERE, "libcbtm.so")
 
 PRM_WORDS = 23
 STATS_WORDS = 32

@@ -513,7 +513,9 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
             const int32_t nx = p.nexts[s], pv = p.prevs[s];
             // the twin rides along: a split's chain walk starts from it (one round trip less per walk)
             // and the apply phase wants it (carried)
-            const int32_t tw = (fast || carry) ? p.twins[s] : kNoTwinYet;
+            // (only for the CTA's first chunk: with many chunks per CTA -- 10^6 live bisectors -- a fourth
+            // scattered load for everybody costs more than the walks of the few that split gain)
+            const int32_t tw = (carry && chunk == bid) ? p.twins[s] : kNoTwinYet;
             // what a merge request will ask about its sibling and the opposite pair: with the LOD
             // classifier gathered now, for everybody, so that the round trip hides behind the fp64 work;
             // the other verdict sources are known at once, so only merge requests gather (three scattered
@@ -1508,8 +1510,11 @@ __device__ __forceinline__ void apply_merged_pair(ApplyCtx &cx, int32_t e, int32
 // bisectors a frame consumes are not spread evenly over the ranks -- 38 .. 93 per chunk on average, 256 in
 // the fullest chunks of the Earth sweep, benchmarks/apply_imbalance.py -- but a balanced deal gives up the
 // carried values, and the two round trips that costs outweigh the balance: 5.4 vs 4.9 us.)
+// skip_quiet_warps: for kernels whose CTAs work through many chunks (wide grid, batches) -- most warps of a
+// quiet frame flip nothing and skip the shuffles of stage 8 with one vote; in the latency-bound frame of a
+// single planet the vote and its branch cost more (apply 4.9 -> 5.2 us) than they can save
 __device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t n, uint32_t bid, uint32_t nb,
-                                            Carry *carry = nullptr)
+                                            Carry *carry = nullptr, bool skip_quiet_warps = true)
 {
     __shared__ uint32_t poisoned;
     const cbtm_pool &p = a.pool;
@@ -1548,7 +1553,9 @@ __device__ __forceinline__ void phase_apply(const FrameArgs &a, uint32_t n, uint
         const uint32_t sm = cmd & CBTM_CMD_SPLIT_MASK;
         // stage 8 first, by the whole warp (kernels.py:598-632): a bisector that splits or belongs to an
         // agreed merge frees its slot, the first na reserved slots come alive
-        warp_flip_bits(bits32, (valid && (sm || mref >= 0)) ? s : -1, na, own.res, tid & 31);
+        const bool consumed = valid && (sm || mref >= 0);
+        if (!skip_quiet_warps || __any_sync(FULL_MASK, consumed || na != 0)) // (warp-uniform)
+            warp_flip_bits(bits32, consumed ? s : -1, na, own.res, tid & 31);
         if (na == 0) continue; // not allocating: untouched, or a non-owner member of an agreed merge
         // A warp holds splitting bisectors and owners of agreed merges side by side, and the two kinds
         // need different things: the split's three neighbour bundles and their parents; the merge's other
@@ -1722,7 +1729,10 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         if (stamp) stamp[1] = global_ns();
         const uint32_t n = p.counters[1];      // the frame's live count: one read per CTA, kept in a register
         const bool fast = fits_a_priori(p, n); // grid-uniform
-        Carry *carry = reinterpret_cast<Carry *>(dyn_smem); // (the staging area of the index phase is free until P6)
+        // (the staging area of the index phase is free until P6; the wide-grid variant goes without: its CTAs
+        // work through many chunks, only the first could be carried, and at 64 registers the extra live
+        // values spill -- measured at 2 M live bisectors: 87 us per frame without, 93 us with)
+        Carry *carry = CTAS == 2 ? reinterpret_cast<Carry *>(dyn_smem) : nullptr;
         phase_classify(a, n, bid, nb, (mailbox && f > 0) ? ctl->mb_prm : nullptr, carry);
         WORK_END(ctl, 1);
         grid.sync();
@@ -1765,7 +1775,7 @@ k_frames(const __grid_constant__ FrameArgs a, int n_frames, int64_t *stats_seq, 
         grid.sync();
         if (stamp) stamp[4] = global_ns();
         PROBE_T0(4, f);
-        phase_apply(a, n, bid, nb, carry);
+        phase_apply(a, n, bid, nb, carry, CTAS != 2);
         PROBE(20); // apply done
         WORK_END(ctl, 4);
         grid.sync();
