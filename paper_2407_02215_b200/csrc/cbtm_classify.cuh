@@ -56,13 +56,11 @@ __device__ __forceinline__ double dot3_rn(double x, double y, double z, double a
     return __dadd_rn(__dadd_rn(__dmul_rn(x, a), __dmul_rn(y, b)), __dmul_rn(z, c));
 }
 
-// 0 keep / 1 split / 2 merge.  prm layout: include/cbtm.h (LodDecide._prm).
-__device__ __forceinline__ int lod_verdict(uint64_t id, int rank, int depth_limit,
-                                           const double *__restrict__ root_tris,
-                                           const double *__restrict__ prm)
+// 0 keep / 1 split / 2 merge from the decoded triangle t (modified in place).  prm layout: include/cbtm.h
+// (LodDecide._prm).
+__device__ __forceinline__ int lod_verdict_of_triangle(double *t, uint64_t id, int rank, int depth_limit,
+                                                       const double *__restrict__ prm)
 {
-    double t[9];
-    decode_triangle(id, rank, root_tris, t);
     const double radius = prm[18];
     if (radius > 0.0) { // radial projection onto the planet, lod.py:185-191
 #pragma unroll
@@ -134,6 +132,15 @@ __device__ __forceinline__ int lod_verdict(uint64_t id, int rank, int depth_limi
     if (area > prm[16]) return depth_of(id, rank) < depth_limit ? 1 : 0;
     if (area < prm[17]) return 2;
     return 0;
+}
+
+__device__ __forceinline__ int lod_verdict(uint64_t id, int rank, int depth_limit,
+                                           const double *__restrict__ root_tris,
+                                           const double *__restrict__ prm)
+{
+    double t[9];
+    decode_triangle(id, rank, root_tris, t);
+    return lod_verdict_of_triangle(t, id, rank, depth_limit, prm);
 }
 
 // bisector.py:154-173 -- root bisector of each halfedge: v0, v1 and the mean

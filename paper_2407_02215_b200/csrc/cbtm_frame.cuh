@@ -213,7 +213,8 @@ struct MergeCfg {
 // js = ids[sib], jo = ids[oth], j4 = next-or-prev[oth]; only ids[j4] is still
 // to be fetched, and only for a quad.
 __device__ __forceinline__ MergeCfg merge_config_gathered(const cbtm_pool &p, uint64_t j1, int32_t sib, int32_t oth,
-                                                          uint64_t js, uint64_t jo, int32_t j4)
+                                                          uint64_t js, uint64_t jo, int32_t j4,
+                                                          const uint64_t *id_j4 = nullptr /* ids[j4], if fetched already */)
 {
     MergeCfg c = {0, -1, -1, -1, 0, 0, 0};
     if (depth_of(j1, p.rank) < 1) return c; // roots never merge
@@ -227,7 +228,7 @@ __device__ __forceinline__ MergeCfg merge_config_gathered(const cbtm_pool &p, ui
     }
     if (bit_length64(jo) != bit_length64(j1)) return c;
     if (j4 < 0) return c;
-    const uint64_t j4id = p.ids[j4];
+    const uint64_t j4id = id_j4 ? *id_j4 : p.ids[j4];
     if ((j4id >> 1) != (jo >> 1)) return c;
     c.kind = 2;
     c.oth = oth;
@@ -545,12 +546,25 @@ __device__ __forceinline__ void phase_classify(const FrameArgs &a, uint32_t n, u
         if (i < n) {
             const uint64_t id = gathered.id, js = gathered.js, jo = gathered.jo;
             const int32_t sib = gathered.sib, oth = gathered.oth, j4 = gathered.j4;
-            const int v = verdict_of(a, prm, id, i);
+            // LOD: the id of a quad's fourth member -- the one gather that hangs on the gathers above -- is
+            // fetched between the decode and the projection, so that it too hides behind fp64 work
+            // instead of following the verdict
+            int v;
+            uint64_t id_j4 = 0;
+            const bool j4_early = a.vmode == CBTM_VERDICT_LOD;
+            if (j4_early) {
+                double tri[9];
+                decode_triangle(id, p.rank, a.root_tris, tri);
+                if (j4 >= 0) id_j4 = p.ids[j4];
+                v = lod_verdict_of_triangle(tri, id, p.rank, p.max_depth, prm);
+            } else {
+                v = verdict_of(a, prm, id, i);
+            }
             if (v == 1) {
                 const int d = depth_of(id, p.rank);
                 if (d < p.max_depth) need = 3 * d + 4;
             } else if (v == 2) {
-                const MergeCfg c = merge_config_gathered(p, id, sib, oth, js, jo, j4);
+                const MergeCfg c = merge_config_gathered(p, id, sib, oth, js, jo, j4, j4_early ? &id_j4 : nullptr);
                 if (c.kind) {
                     need = 2;
                     mbits = CBTM_CMD_MERGE;
