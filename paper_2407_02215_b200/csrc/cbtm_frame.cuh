@@ -1419,8 +1419,7 @@ __device__ __forceinline__ void warp_flip_bits(const BitSink &b, int32_t freed, 
         if (slot[k] >= 0) set_live(b, slot[k]);
 }
 
-// kernels.py:373-461 restated over the two halves of the bisector
-// a consumed bisector's own record, fetched together with its command word
+// a consumed bisector's own record, fetched together with its command word (or carried)
 struct OwnRecord {
     uint64_t id;
     int32_t nx, pv, tw;
