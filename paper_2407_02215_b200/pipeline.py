@@ -75,6 +75,15 @@ class UpdateStats:
             # t6 = fused fill/neighbours/bitfield; t9 = reduction (+ stats publish)
             times = [0, ph[0] // 1000, 0, ph[1] // 1000, (ph[2] + ph[3]) // 1000, ph[4] // 1000,
                      0, 0, ph[5] // 1000]
+        elif times is not None and (ph[1] or ph[2]):
+            # host-evaluated verdicts, profiled: stages 1-2 by events around cbtm_update_begin (slot 1), the
+            # verdict evaluation on the host by events (slot 3 arrives as the begin -> finish span), and the
+            # device's own phase timers of cbtm_update_finish for the stages behind it
+            times = list(times)
+            host_span = times[3]
+            device_us = [ph[1] // 1000, (ph[2] + ph[3]) // 1000, ph[4] // 1000, ph[5] // 1000]
+            times[3] = max(0, host_span - sum(device_us)) + device_us[0]   # t4: verdicts (host) + generate commands
+            times[4], times[5], times[8] = device_us[1], device_us[2], device_us[3]
         else:
             ph = [0] * _N_PHASES
             times = list(times) if times is not None else [0] * 9
