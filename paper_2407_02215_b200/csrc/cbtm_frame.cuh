@@ -1056,10 +1056,20 @@ __device__ __forceinline__ void phase_reserve(const FrameArgs &a, uint32_t n, ui
 
     long long off = 0;      // slots allocated by chunks [0, summed)
     uint32_t summed = 0;
-    for (uint32_t chunk = bid; chunk < nch; chunk += nb) {
+    uint32_t totals = 0; // lane k: the count of the k-th of this CTA's next 32 chunks (one round trip for 32 of them)
+    for (uint32_t chunk = bid, k32 = 0; chunk < nch; chunk += nb, k32 = (k32 + 1) & 31u) {
         // one round trip: the chunk's own count, this rank's count and slot, and the counts of the
         // chunks between the previous chunk of this CTA and this one
-        const uint32_t total = a.ws.chunk_alloc[chunk];
+        if (k32 == 0) {
+            const uint64_t mine = chunk + (uint64_t)lane * nb;
+            totals = mine < nch ? a.ws.chunk_alloc[mine] : 0u;
+        }
+        const uint32_t total = __shfl_sync(FULL_MASK, totals, (int)k32);
+        // A CTA with many chunks (10^5 .. 10^7 live bisectors) does not sum the counts in front of a chunk
+        // that allocates nothing: the sum is caught up by the next chunk that does (most chunks of a quiet
+        // frame allocate nothing, and every sum is a round trip and two CTA barriers).  With one chunk per
+        // CTA the sum is issued together with `total` instead of behind it.
+        if (nch > nb && total == 0) continue; // CTA-uniform
         const uint32_t i = chunk * CHUNK + tid;
         const bool carried = carry && chunk == bid; // CTA-uniform
         const uint32_t na = i < n ? (carried ? carry->na[tid] : a.ws.nalloc8[i]) : 0;
