@@ -357,6 +357,17 @@ def cbt_kernel_probe(L, torch, device, depth, bits, peak, cpu_pool=None, cpu_thr
 
     red_ms = _time_graph(torch, device, flush, reduce, copies)
     red_single_ms = _time_single(torch, device, flush, reduce)
+    # a longer series (32 launches on 32 cold copies): the first launch of a series has nothing to overlap
+    # with and the graph launch itself costs a few microseconds -- an eighth of that is in `us` above
+    long_series = None
+    if depth <= 28:
+        copies32 = 32
+        bits_k += [bits.clone() for _ in range(copies32 - copies)]
+        cnts += [cnts[0].clone() for _ in range(copies32 - copies)]
+        long_ms = _time_graph(torch, device, flush, reduce, copies32, reps=9)
+        del bits_k[copies:], cnts[copies:]
+        torch.cuda.empty_cache()
+        long_series = {"launches": copies32, "us": long_ms * 1e3}
     ones = int(cnts[0][1].item())
     live = torch.empty(n, dtype=torch.int32, device=device)
     free = torch.empty(n, dtype=torch.int32, device=device)
@@ -372,6 +383,8 @@ def cbt_kernel_probe(L, torch, device, depth, bits, peak, cpu_pool=None, cpu_thr
     out = {"leaves": n, "occupancy": ones / n,
            "reduce": {"us": red_ms * 1e3, "GB/s": red_bytes / red_ms / 1e6, "frac": red_bytes / red_ms / 1e6 / peak,
                       "algorithmic_bytes": red_bytes, "single_launch_us": red_single_ms * 1e3,
+                      "series_of_32": None if long_series is None else dict(
+                          long_series, frac=red_bytes / (long_series["us"] * 1e-6) / 1e9 / peak),
                       "timing": f"{copies} launches on {copies} cold copies as one CUDA graph, per launch, median of 15"},
            "decode_all": {"us": idx_ms * 1e3, "GB/s": all_bytes / idx_ms / 1e6,
                           "frac": all_bytes / idx_ms / 1e6 / peak, "algorithmic_bytes": all_bytes,

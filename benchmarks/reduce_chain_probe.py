@@ -27,7 +27,7 @@ dev = torch.device("cuda", 0)
 flush = torch.zeros(512 << 20, dtype=torch.uint8, device=dev)
 ws = torch.zeros(2048, dtype=torch.uint8, device=dev)
 base = (ws.data_ptr() + 1023) // 1024 * 1024
-NL = 4     # (the debug build keeps the stamps of four launches: slots by ticket address)
+NL = int(os.environ.get("CHAIN", "4"))     # launches per series; the debug build keeps the stamps of the LAST four (slots by ticket address)
 WARM = "--warm" in sys.argv     # no L2 flush between the repetitions: everything the launches read sits in L2
 for depth in [int(a) for a in sys.argv[1:] if a.isdigit()] or [24, 26, 28]:
     bits = [device_bits(depth, 0.5, False, dev)]
@@ -55,13 +55,13 @@ for depth in [int(a) for a in sys.argv[1:] if a.isdigit()] or [24, 26, 28]:
     tiles = max(1, (1 << depth) >> 17)
     st = np.zeros((4 * 2048, 5), dtype=np.uint64)
     assert L.cbtm_debug_reduce_stamps(st.ctypes.data, 4 * 2048) == 0
-    rows = [st[k * 2048:(k + 1) * 2048] for k in range(NL)]
+    rows = [st[(k % 4) * 2048:(k % 4 + 1) * 2048] for k in range(NL - 4, NL)]
     rows = [r[r[:, 0] > 0] for r in rows]
     t0 = min(int(r[:, 0].min()) for r in rows)
-    sm_load = np.bincount(rows[1][:, 4].astype(np.int64), minlength=148)
+    sm_load = np.bincount(rows[-1][:, 4].astype(np.int64), minlength=148)
     print(f"D={depth}: {tiles} tiles, {len(rows[0])} CTAs, graph of {NL}: {a.elapsed_time(b) * 1e3 / NL:.2f} us per launch; "
           f"CTAs per SM of launch 1: min {sm_load[sm_load > 0].min()} max {sm_load.max()} on {int((sm_load > 0).sum())} SMs")
-    for k, r in enumerate(rows):
+    for k, r in enumerate(rows, NL - 4):
         rel = (r[:, :4].astype(np.int64) - t0) / 1e3
         print(f"   launch {k}: entry {rel[:, 0].min():6.2f}..{rel[:, 0].max():6.2f}  released {rel[:, 1].min():6.2f}/"
               f"{np.median(rel[:, 1]):6.2f}/{rel[:, 1].max():6.2f}  first tile {rel[:, 2].min():6.2f}/{np.median(rel[:, 2]):6.2f}/"

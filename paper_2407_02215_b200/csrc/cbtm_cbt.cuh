@@ -353,7 +353,6 @@ k_sum_reduce(const uint8_t *bits, uint32_t *counters, int lc, uint64_t total_byt
     const uint8_t *src = bits + (size_t)tile * RED_TILE_BYTES;
 
     RED_STAMP(0);
-    griddep_launch_dependents();
     // nothing is READ before the wait: the address comes from the launch parameters, and a line
     // prefetched into L2 cannot go stale (L2 is where the previous kernel's writes land)
     if (t == 0 && prefetch) bulk_prefetch_l2(src, bytes);
@@ -384,6 +383,12 @@ k_sum_reduce(const uint8_t *bits, uint32_t *counters, int lc, uint64_t total_byt
 #pragma unroll
         for (int j = 0; j < 16; ++j) w[j] = 0;
     }
+    // The next grid of the stream may be set up from here on -- not earlier: a CTA that waits in
+    // griddepcontrol.wait holds its slot, and in a long series of reductions the grids two and three ahead
+    // (each released as soon as all CTAs of the one before it were running) piled up on the SMs, left the
+    // current grid a CTA or two per SM and made a launch 4.3 us long (benchmarks/reduce_chain_probe.py with
+    // CHAIN=16: 1..7 CTAs of one grid per SM).  Triggered behind the wait, only ONE grid is ever waiting.
+    griddep_launch_dependents();
     const int top = lc - 7; // level of the tile roots (n_tiles > 1)
     uint32_t old_root = 0;
     // The stamp is the same word for every CTA of the grid (only the rebuild path writes it, after the
