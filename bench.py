@@ -376,6 +376,9 @@ def cbt_kernel_probe(L, torch, device, depth, bits, peak, cpu_pool=None, cpu_thr
         assert L.cbtm_index(bits.data_ptr(), cnts[0].data_ptr(), depth, live.data_ptr(), free.data_ptr(), 0, stream) == 0
 
     idx_ms = _time_single(torch, device, flush, index, reps=5)
+    # back to back (one graph of 4 launches on the same buffers: every launch writes 4 N bytes, far more than
+    # the L2 holds, so each one starts cold): without the launch overhead of a lone, event-timed kernel
+    idx_series_ms = _time_graph(torch, device, flush, index, 4, reps=5)
     # spot check: the compacted lists are sorted and partition the pool
     assert bool((live[1:ones] > live[:ones - 1]).all()) and bool((free[1:n - ones] > free[:n - ones - 1]).all())
     red_bytes = n // 8 + 4 * L.cbtm_counter_words(depth)
@@ -388,6 +391,7 @@ def cbt_kernel_probe(L, torch, device, depth, bits, peak, cpu_pool=None, cpu_thr
                       "timing": f"{copies} launches on {copies} cold copies as one CUDA graph, per launch, median of 15"},
            "decode_all": {"us": idx_ms * 1e3, "GB/s": all_bytes / idx_ms / 1e6,
                           "frac": all_bytes / idx_ms / 1e6 / peak, "algorithmic_bytes": all_bytes,
+                          "series_of_4": {"us": idx_series_ms * 1e3, "frac": all_bytes / idx_series_ms / 1e6 / peak},
                           "timing": "single launch, CUDA events, median of 5"}}
     if cpu_pool is not None:
         import ctypes as C
