@@ -437,16 +437,28 @@ int cbtm_export_live_triangles(const cbtm_pool *pool, const double *root_tris, d
     if (out_capacity < 0) return CBTM_E_RANGE;
     cudaStream_t st = as_stream(stream);
     // the active list of the CURRENT state (an update leaves the list of the state it started from)
-    k_index<false><<<strided_grid(make_geo(pool->depth).nblocks, IDX_WARPS, 6), IDX_WARPS * 32, 0, st>>>(
-        reinterpret_cast<const uint32_t *>(pool->bits), pool->counters, pool->depth, pool->cache_live, nullptr,
-        pool->dispatch, nullptr);
-    rc = launch_status();
+    // both launches with programmatic stream serialization: each grid is set up while the kernel before it
+    // on the stream (the frame kernel; the index pass) drains, and waits in griddepcontrol.wait
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(strided_grid(make_geo(pool->depth).nblocks, IDX_WARPS, 6));
+    cfg.blockDim = dim3(IDX_WARPS * 32);
+    rc = status(cudaLaunchKernelEx(&cfg, k_index<false>, reinterpret_cast<const uint32_t *>(pool->bits),
+                                   (const uint32_t *)pool->counters, (int)pool->depth, pool->cache_live, (int32_t *)nullptr,
+                                   pool->dispatch, (uint32_t *)nullptr));
     if (rc) return rc;
     const uint64_t cap = (uint64_t)out_capacity < ((uint64_t)1 << pool->depth) ? (uint64_t)out_capacity
                                                                                : ((uint64_t)1 << pool->depth);
-    k_export_live_triangles<<<strided_grid(cap ? cap : 1, 256, 8), 256, 0, st>>>(
-        pool->ids, pool->cache_live, pool->counters, pool->rank, root_tris, out, (uint64_t)out_capacity, draw_args);
-    return launch_status();
+    cfg.gridDim = dim3(strided_grid(cap ? cap : 1, 256, 8));
+    cfg.blockDim = dim3(256);
+    return status(cudaLaunchKernelEx(&cfg, k_export_live_triangles, (const uint64_t *)pool->ids,
+                                     (const int32_t *)pool->cache_live, (const uint32_t *)pool->counters, (int)pool->rank,
+                                     root_tris, out, (uint64_t)out_capacity, draw_args));
 }
 
 int cbtm_validate(const cbtm_pool *pool, int32_t n_halfedges, int64_t *out, uintptr_t stream)

@@ -906,6 +906,8 @@ k_index(const uint32_t *bits32, const uint32_t *counters, int depth, int32_t *ca
         int32_t *cache_free, uint32_t *dispatch, uint32_t *reset_cmds)
 {
     __shared__ __align__(16) int32_t stage[IDX_WARPS][IDX_STAGE_WORDS];
+    griddep_wait(); // (no-ops unless launched with programmatic stream serialization: cbtm_export_live_triangles)
+    griddep_launch_dependents();
     index_phase<RESET>(bits32, counters, depth, cache_live, cache_free, dispatch, reset_cmds, stage, blockIdx.x,
                        gridDim.x);
 }

@@ -194,6 +194,9 @@ k_export_live_triangles(const uint64_t *__restrict__ ids, const int32_t *__restr
                         const uint32_t *__restrict__ counters, int rank, const double *__restrict__ root_tris,
                         double *__restrict__ out, uint64_t out_capacity, uint32_t *__restrict__ draw_args)
 {
+    // (launched with programmatic stream serialization behind the index pass: set up while that one drains)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint32_t n = counters[1];
     const uint64_t m = n < out_capacity ? n : out_capacity;
     if (blockIdx.x == 0 && threadIdx.x == 0 && draw_args) {
